@@ -1,0 +1,486 @@
+"""B200 benchmark: AES-128 encrypt GB/s of plaintext (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+A "step" is one pass of the hot path over one batch: encrypt every block of
+the configured workload once (shared-IV CBC over 16-byte messages, i.e.
+C_i = AES_K(P_i ^ IV), the reference's mode).
+
+* ``value``   -- whole-job plaintext GB/s, inputs resident in HBM, CUDA events
+                 on the launching stream, max over ranks.
+* ``e2e``     -- the same metric through the public host-buffer API
+                 (``backend_cuda.encrypt_shared_iv`` -> C ABI
+                 ``gaes_encrypt_shared_iv``) with pinned host input/output:
+                 H2D + kernel + D2H inside the timed region every step.
+* ``roofline``-- binding roofline of the dominant kernel (shared-memory
+                 table lookups, 160 per block) plus the HBM roofline
+                 (32 algorithmic bytes per block) for reference.
+* ``cpu_baseline`` -- the reference's own compiled kernel (oracle/_ref,
+                 built from pkg/src/gaes/_kernel.pyx) on the host cores, rank 0
+                 at N=1, on a bounded sample.
+
+Workloads (BASELINE.json configs, seeded synthetic data generated on device):
+  1: 2^16 uniform blocks per GPU (weak)     2: 2^24 uniform blocks per GPU (weak, default)
+  3: 2^28 sensor-stream blocks, sharded     4: 2^26 Zipf(1.1) uint64 blocks, sharded
+  5: 1024 keys x 2^20 blocks, keys sharded (strong)
+``--impl reference`` times the reference CPU kernel instead (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+BYTES_PER_BLOCK = 16
+LOOKUPS_PER_BLOCK = 160  # 9 rounds x 16 T-table lookups + 16 S-box lookups
+HBM_BYTES_PER_BLOCK = 32  # 16 read + 16 written (shared IV folded into the key)
+SEED = 2016  # bench.py:49 default seed in the reference
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline budget")
+    ap.add_argument("--variant", type=int, default=0)
+    return ap.parse_args()
+
+
+WORKLOADS = {
+    1: dict(name="cfg1: 2^16 uniform 16-B blocks per GPU, one key, shared IV", blocks=1 << 16, scaling="weak"),
+    2: dict(name="cfg2: 2^24 uniform 16-B blocks (256 MiB) per GPU, one key, shared IV", blocks=1 << 24,
+            scaling="weak"),
+    3: dict(name="cfg3: 2^28 sensor-stream blocks (4 GiB) sharded over GPUs, one key", blocks=1 << 28,
+            scaling="strong"),
+    4: dict(name="cfg4: 2^26 Zipf(1.1) uint64 column blocks (1 GiB) sharded, one key", blocks=1 << 26,
+            scaling="strong"),
+    5: dict(name="cfg5: 1024 keys x 2^20 blocks (16 GiB), keys sharded, GPU key schedule", blocks=1 << 30,
+            scaling="strong", keys=1024),
+}
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.reader = threading.Thread(target=self._read, daemon=True)
+            self.reader.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.reader.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max((float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()),
+                                   default=None)}
+
+
+# ----------------------------------------------------------------------------- inputs
+
+def make_inputs(cfg: int, rank: int, world: int, device):
+    """Seeded synthetic plaintext for this rank, generated on the device."""
+    import torch
+    from paper_1506_08503_b200.shard import key_slice, rank_slice
+
+    w = WORKLOADS[cfg]
+    rng = np.random.default_rng(SEED)
+    key, iv = rng.bytes(16), rng.bytes(16)  # bench.py:124-125 draw order
+    gen = torch.Generator(device=device)
+    gen.manual_seed(SEED * 1000 + rank)
+    meta = {"seed": SEED, "key": key.hex(), "iv": iv.hex()}
+    if cfg in (1, 2):
+        n = w["blocks"]
+        p = torch.randint(0, 256, (n, 16), dtype=torch.uint8, device=device, generator=gen)
+        return dict(p=p, key=key, iv=iv, meta=meta)
+    if cfg == 3:
+        lo, hi = rank_slice(w["blocks"], rank, world)
+        n = hi - lo
+        f = rng.uniform(0.001, 0.1, 3)
+        a = rng.uniform(1000, 8000, 3)
+        phi = rng.uniform(0, 2 * np.pi, 3)
+        meta.update(freqs=f.tolist(), amps=a.tolist(), phases=phi.tolist(), sigma=200)
+        p = torch.empty((n, 16), dtype=torch.uint8, device=device)
+        samples = p.view(torch.int16).view(-1)  # 8 LE int16 per block
+        chunk = 1 << 26
+        t0 = lo * 8
+        for s in range(0, samples.numel(), chunk):
+            e = min(samples.numel(), s + chunk)
+            t = torch.arange(t0 + s, t0 + e, dtype=torch.float64, device=device)
+            x = torch.zeros_like(t)
+            for k in range(3):
+                x += a[k] * torch.sin(2 * np.pi * f[k] * t + phi[k])
+            x += 200.0 * torch.randn(t.shape, dtype=torch.float64, device=device, generator=gen)
+            samples[s:e] = torch.clamp(torch.round(x), -32768, 32767).to(torch.int16)
+        return dict(p=p, key=key, iv=iv, meta=meta)
+    if cfg == 4:
+        lo, hi = rank_slice(w["blocks"], rank, world)
+        n = hi - lo
+        nvals = 10 ** 6
+        vals = np.unique(rng.integers(0, 2 ** 64, int(nvals * 1.05), dtype=np.uint64))
+        vals = rng.permutation(vals)[:nvals]
+        ranks_w = np.arange(1, nvals + 1, dtype=np.float64) ** -1.1
+        cdf = torch.from_numpy(np.cumsum(ranks_w) / ranks_w.sum()).to(device)
+        u = torch.rand(n, dtype=torch.float64, device=device, generator=gen)
+        r = torch.searchsorted(cdf, u).clamp_(max=nvals - 1)
+        v = torch.from_numpy(vals.view(np.int64)).to(device)[r]
+        p = torch.zeros((n, 16), dtype=torch.uint8, device=device)
+        p[:, :8] = v.view(torch.uint8).view(n, 8)
+        meta.update(zipf_s=1.1, distinct=nvals)
+        return dict(p=p, key=key, iv=iv, meta=meta)
+    # cfg 5: many keys
+    k_lo, k_hi = key_slice(w["keys"], rank, world)
+    keys = rng.integers(0, 256, (w["keys"], 16), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (w["keys"], 16), dtype=np.uint8)
+    bpk = w["blocks"] // w["keys"]
+    n = (k_hi - k_lo) * bpk
+    p = torch.randint(0, 256, (n, 16), dtype=torch.uint8, device=device, generator=gen)
+    return dict(p=p, key=key, iv=iv, keys=keys[k_lo:k_hi], ivs=ivs[k_lo:k_hi], bpk=bpk, meta=meta)
+
+
+# ----------------------------------------------------------------------------- CPU reference
+
+def _ref_kernel():
+    """The reference's own compiled kernel (oracle/_ref, from _kernel.pyx)."""
+    sys.path.insert(0, os.path.join(REPO, "oracle", "_ref"))
+    try:
+        import _kernel  # type: ignore
+        return _kernel, "reference"
+    except ImportError:
+        return None, "port"
+    finally:
+        sys.path.pop(0)
+
+
+def cpu_reference_rate(key: bytes, iv: bytes, n: int, threads: int, reps: int = 1, warm: int = 1):
+    """Encrypt n blocks on the host with the reference kernel over `threads`
+    contiguous chunks (parallel._run_chunks, parallel.py:66-75).  Returns
+    (list of per-rep seconds, kind)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle
+    kern, kind = _ref_kernel()
+    rng = np.random.default_rng(SEED + 1)
+    p = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (n, 1))
+    out = np.empty_like(p)
+    tables = oracle.encrypt_tables(key)
+    chunks = oracle.plan(n, threads)
+
+    def run_once():
+        if kern is None:
+            oracle.cbc_encrypt(p, ivrows, *tables, out, threads=threads)
+            return
+        if len(chunks) <= 1:
+            kern.cbc_encrypt(p, ivrows, *tables, out)
+            return
+        with ThreadPoolExecutor(max_workers=len(chunks)) as pool:
+            fs = [pool.submit(kern.cbc_encrypt, p[lo:hi], ivrows[lo:hi], *tables, out[lo:hi])
+                  for lo, hi in chunks]
+            for f in fs:
+                f.result()
+
+    for _ in range(warm):
+        run_once()
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        run_once()
+        times.append(time.perf_counter() - t0)
+    # the sample is checked: the CPU leg must compute the same bytes
+    want = oracle.encrypt(key, ivrows[:256], p[:256])
+    assert np.array_equal(out[:256], want), "CPU reference disagrees with the oracle"
+    return times, kind
+
+
+def cpu_baseline(key, iv, budget_s: float):
+    threads = os.cpu_count() or 1
+    probe_n = 1 << 16
+    t, kind = cpu_reference_rate(key, iv, probe_n, threads, reps=1, warm=1)
+    rate = probe_n / max(t[0], 1e-9)
+    n = int(min(1 << 26, max(probe_n, rate * budget_s / 2)))
+    times, kind = cpu_reference_rate(key, iv, n, threads, reps=2, warm=0)
+    sec = statistics.median(times)
+    return {"value": n * BYTES_PER_BLOCK / sec / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": f"{n} uniform 16-B blocks (shared IV, seed {SEED + 1}), median of 2 reps, "
+                      f"{threads} threads over parallel.plan chunks"}
+
+
+def run_reference_impl(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return 0
+    w = WORKLOADS[args.config]
+    rng = np.random.default_rng(SEED)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    threads = os.cpu_count() or 1
+    probe_n = 1 << 16
+    t, kind = cpu_reference_rate(key, iv, probe_n, threads)
+    rate = probe_n / max(t[0], 1e-9)
+    budget_per_step = 120.0 / max(1, args.steps + args.warmup)
+    n = int(min(w["blocks"] if args.config != 5 else 1 << 20, max(probe_n, rate * budget_per_step)))
+    times, kind = cpu_reference_rate(key, iv, n, threads, reps=args.steps, warm=args.warmup)
+    total = sum(times)
+    value = n * args.steps * BYTES_PER_BLOCK / total / 1e9
+    sample = (f"{n} of the workload's uniform 16-B blocks per step, {threads} host threads "
+              f"(oracle/_ref = reference _kernel.pyx compiled, parallel.plan chunks)")
+    line = {
+        "impl": "reference", "metric": "AES-128 encrypt GB/s of plaintext", "value": value, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": w["scaling"], "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded uniform bytes)",
+        "config": {"workload": w["name"], "sample_blocks_per_step": n, "parallelism": f"{threads} host threads"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- ours
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_impl(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle  # checker only (outside the timed region)
+    from paper_1506_08503_b200 import _lib, backend_cuda, device
+    from paper_1506_08503_b200.shard import max_over_ranks
+
+    rank = int(os.environ.get("RANK", 0))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if args.variant:
+        _lib.check(_lib.lib().gaes_set_variant(args.variant))
+
+    w = WORKLOADS[args.config]
+    inp = make_inputs(args.config, rank, world, dev)
+    p = inp["p"]
+    n = p.shape[0]
+    key, iv = inp["key"], inp["iv"]
+    rk = device.expand_key(key, dev)
+    assert np.array_equal(rk, oracle.gen_keys(key)), "GPU key schedule disagrees with the oracle"
+    out = torch.empty_like(p)
+    stream = torch.cuda.current_stream()
+
+    if args.config == 5:
+        d_keys = torch.from_numpy(inp["keys"]).to(dev)
+        d_ivs = torch.from_numpy(inp["ivs"]).to(dev)
+        rk_enc, rk_dec = device.expand_keys(d_keys)
+        assert np.array_equal(rk_enc.cpu().numpy(), oracle.gen_keys_batch(inp["keys"])), "key schedule mismatch"
+
+        def step():
+            device.many_key_encrypt(p, rk_enc, d_ivs, out=out)
+    else:
+        def step():
+            device.encrypt_blocks(p, rk, iv, out=out)
+
+    flush = None
+    if n * 32 < 256 << 20:  # working set below 2x L2: flush L2 between timed steps
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: per-step CUDA events on the launching stream
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = _lib.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.fill_(i & 0xFF)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = _lib.launch_count() - launches0
+    ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_local = sum(ms) / len(ms)
+    ms_step = max_over_ranks(ms_local, dev)
+    total_blocks = n * world if w["scaling"] == "weak" else w["blocks"]
+    if w["scaling"] == "strong" and world == 1:
+        total_blocks = n
+    value = total_blocks * BYTES_PER_BLOCK / (ms_step / 1e3) / 1e9
+    clocks = clk.summary()
+
+    # ---- verification (outside the timed region): sample vs the oracle, round trip
+    ph = p[:4096].cpu().numpy()
+    ch = out[:4096].cpu().numpy()
+    if args.config == 5:
+        bpk = inp["bpk"]
+        k0 = inp["keys"][0].tobytes()
+        ivrows = np.tile(inp["ivs"][0], (min(4096, bpk), 1))
+        verified = bool(np.array_equal(ch[:ivrows.shape[0]], oracle.encrypt(k0, ivrows, ph[:ivrows.shape[0]])))
+        back = device.many_key_decrypt(out, rk_dec, d_ivs)
+    else:
+        ivrows = np.tile(np.frombuffer(iv, np.uint8), (4096, 1))
+        verified = bool(np.array_equal(ch, oracle.encrypt(key, ivrows, ph)))
+        idx = torch.randint(0, n, (4096,), device=dev)
+        ps, cs = p[idx].cpu().numpy(), out[idx].cpu().numpy()
+        verified &= bool(np.array_equal(cs, oracle.encrypt(key, ivrows, ps)))
+        back = device.decrypt_blocks(out, rk, iv)
+    verified &= bool(torch.equal(back, p))
+
+    # decrypt throughput (reported, not the metric)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(3):
+        if args.config == 5:
+            device.many_key_decrypt(out, rk_dec, d_ivs, out=back)
+        else:
+            device.decrypt_blocks(out, rk, iv, out=back)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    dec_gbs = n * BYTES_PER_BLOCK / (ev0.elapsed_time(ev1) / 3 / 1e3) / 1e9
+
+    # ---- e2e through the public host-buffer API (pinned host memory)
+    e2e = None
+    if not args.no_e2e and args.config != 5:
+        n_e2e = n
+        h_in = torch.empty((n_e2e, 16), dtype=torch.uint8).pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        h_in.copy_(p[:n_e2e])
+        hi, ho = h_in.numpy(), h_out.numpy()
+        for _ in range(2):
+            backend_cuda.encrypt_shared_iv(hi, iv, rk, out=ho)
+        if world > 1:
+            dist.barrier()
+        ts = []
+        for _ in range(max(3, min(args.steps, 10))):
+            t0 = time.perf_counter()
+            backend_cuda.encrypt_shared_iv(hi, iv, rk, out=ho)
+            ts.append(time.perf_counter() - t0)
+        e2e_s = max_over_ranks(sum(ts) / len(ts), dev)
+        e2e_blocks = n_e2e * world if w["scaling"] == "weak" else total_blocks
+        verified &= bool(np.array_equal(ho[:4096], ch[:4096]))
+        e2e = {"value": e2e_blocks * BYTES_PER_BLOCK / e2e_s / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": int(n_e2e * 16), "d2h_bytes_per_step": int(n_e2e * 16),
+               "api": "backend_cuda.encrypt_shared_iv -> gaes_encrypt_shared_iv (pinned host buffers)"}
+
+    # ---- roofline of the dominant kernel (k_blocks encrypt): one launch per step
+    sm_mhz = clocks.get("sm_mhz") or 1965.0
+    peaks = {}
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    per_gpu_blocks_s = n / (ms_local / 1e3)
+    lds_achieved = per_gpu_blocks_s * LOOKUPS_PER_BLOCK / 1e9
+    lds_peak = sms * 32 * sm_mhz * 1e6 / 1e9
+    hbm_achieved = per_gpu_blocks_s * HBM_BYTES_PER_BLOCK / 1e9
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(f"cfg{args.config}")
+        except (OSError, ValueError):
+            traffic = None
+    roofline = {
+        "bound": "smem", "kernel": _lib.last_kernel(),
+        "achieved": round(lds_achieved, 2), "peak": round(lds_peak, 2), "unit": "Glookup/s",
+        "frac": round(lds_achieved / lds_peak, 4), "traffic": traffic,
+        "per_block": f"{LOOKUPS_PER_BLOCK} conflict-free 4-B LDS lookups; peak = {sms} SMs x 32 lanes/clk x "
+                     f"{sm_mhz:.0f} MHz (median SM clock sampled during the timed region)",
+        "hbm": {"achieved": round(hbm_achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(hbm_achieved / hbm_peak, 4),
+                "per_block": f"{HBM_BYTES_PER_BLOCK} B (16 read + 16 written)",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
+    }
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(key, iv, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": "AES-128 encrypt GB/s of plaintext", "value": round(value, 2), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": w["scaling"], "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded, generated on device)",
+            "config": {"workload": w["name"], "blocks_per_gpu": n, "total_blocks": total_blocks,
+                       "l2": "L2 flushed between steps" if flush is not None else
+                             "inputs larger than L2 (no flush)",
+                       "parallelism": f"dp{world} (contiguous block shards, no collective)", **inp["meta"]},
+            "gpu_launches": launches, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+            "decrypt_gbs_per_gpu": round(dec_gbs, 2), "verified": verified,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0 if verified else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

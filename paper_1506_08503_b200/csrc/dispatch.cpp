@@ -1,0 +1,786 @@
+// dispatch.cpp -- host side of libgaes_b200.so: the C ABI (include/gaes_b200.h),
+// per-device contexts, table caching, the H2D -> kernel -> D2H pipeline and
+// the multi-GPU row sharding.
+//
+// Reference boundary replaced: pkg/src/gaes/backend.py:56-61 forwards
+// cbc_encrypt / cbc_decrypt (7 arguments) to the active kernel module;
+// _kernel.pyx:12-101 is the kernel.  parallel.py:37-50 (plan) and :66-75
+// (thread fan-out over contiguous row ranges) become the GPU shard plan.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/gaes_b200.h"
+#include "gf.cuh"
+#include "kernels.h"
+
+using namespace gaes;
+
+namespace {
+
+constexpr int kVersion = 10000;  // 1.0.0
+constexpr uint8_t kShiftRowsSrc[16] = {0, 5, 10, 15, 4, 9, 14, 3, 8, 13, 2, 7, 12, 1, 6, 11};  // aes_cbc.py:41
+constexpr uint8_t kInvShiftRowsSrc[16] = {0, 13, 10, 7, 4, 1, 14, 11, 8, 5, 2, 15, 12, 9, 6, 3};  // :42
+
+thread_local std::string t_err;
+std::atomic<uint64_t> g_launches{0};
+std::mutex g_name_mu;
+std::string g_last_kernel = "";
+std::atomic<int> g_num_gpus{0};
+std::atomic<int> g_variant{0};
+
+int fail(int code, const std::string& msg) {
+  t_err = msg;
+  return code;
+}
+
+#define GAES_CK(expr)                                                                        \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) return fail(GAES_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+void note_kernel(const char* name) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  std::lock_guard<std::mutex> lk(g_name_mu);
+  g_last_kernel = name;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return std::atoi(v);
+}
+
+// --------------------------------------------------------------------------
+// Per-device context.
+struct Slot {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+  uint8_t *h_in = nullptr, *h_out = nullptr, *h_iv = nullptr;  // pinned staging
+  uint8_t *d_in = nullptr, *d_out = nullptr, *d_iv = nullptr;
+  size_t cap = 0, iv_cap = 0;
+  // pending D2H copy-out (pageable destination)
+  uint8_t* pending_dst = nullptr;
+  size_t pending_bytes = 0;
+};
+
+constexpr int kSlots = 3;
+
+struct DevCtx {
+  int dev = 0;
+  int sms = 148;
+  std::mutex mu;  // serialises host-API use of the staging slots
+  uint32_t* d_std_enc = nullptr;  // compact 5x256 (GF layer)
+  uint32_t* d_std_dec = nullptr;
+  uint8_t std_sbox[256], std_inv[256];
+  uint32_t std_te[1024], std_td[1024];
+  std::mutex cache_mu;
+  std::unordered_map<std::string, uint32_t*> cache;  // (box || lut) -> compact tables
+  uint8_t* d_scratch = nullptr;  // box(256) lut(4096) perm(16) rk(176)
+  Slot slots[kSlots];
+};
+
+std::mutex g_ctx_mu;
+std::vector<std::unique_ptr<DevCtx>> g_ctx;
+int g_ndev = -1;
+
+int device_count() {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if (g_ndev < 0) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    g_ndev = n;
+    g_ctx.resize(n);
+  }
+  return g_ndev;
+}
+
+// Creates the context on first use: GF-layer tables built on the device.
+int get_ctx(int dev, DevCtx** out) {
+  const int n = device_count();
+  if (n <= 0) return fail(GAES_ENODEV, "no CUDA device visible");
+  if (dev < 0 || dev >= n) return fail(GAES_EINVAL, "device index out of range");
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if (g_ctx[dev]) {
+    *out = g_ctx[dev].get();
+    return GAES_OK;
+  }
+  auto c = std::make_unique<DevCtx>();
+  c->dev = dev;
+  int prev = 0;
+  GAES_CK(cudaGetDevice(&prev));
+  GAES_CK(cudaSetDevice(dev));
+  GAES_CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
+  GAES_CK(cudaMalloc(&c->d_std_enc, kCompactWords * 4));
+  GAES_CK(cudaMalloc(&c->d_std_dec, kCompactWords * 4));
+  GAES_CK(cudaMalloc(&c->d_scratch, 256 + 4096 + 16 + 176 + 512));
+  uint8_t* d_box = nullptr;
+  int* d_err = nullptr;
+  GAES_CK(cudaMalloc(&d_box, 512));
+  GAES_CK(cudaMalloc(&d_err, sizeof(int)));
+  GAES_CK(cudaMemset(d_err, 0, sizeof(int)));
+  GAES_CK(launch_gf_build(c->d_std_enc, c->d_std_dec, d_box, d_box + 256, d_err, 0));
+  note_kernel("k_gf_build");
+  int err = 0;
+  GAES_CK(cudaMemcpy(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  GAES_CK(cudaMemcpy(c->std_sbox, d_box, 256, cudaMemcpyDeviceToHost));
+  GAES_CK(cudaMemcpy(c->std_inv, d_box + 256, 256, cudaMemcpyDeviceToHost));
+  uint32_t tmp[kCompactWords];
+  GAES_CK(cudaMemcpy(tmp, c->d_std_enc, sizeof(tmp), cudaMemcpyDeviceToHost));
+  std::memcpy(c->std_te, tmp, sizeof(c->std_te));
+  GAES_CK(cudaMemcpy(tmp, c->d_std_dec, sizeof(tmp), cudaMemcpyDeviceToHost));
+  std::memcpy(c->std_td, tmp, sizeof(c->std_td));
+  cudaFree(d_box);
+  cudaFree(d_err);
+  for (auto& s : c->slots) {
+    GAES_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    GAES_CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+  }
+  GAES_CK(cudaSetDevice(prev));
+  if (err) return fail(GAES_ETABLE, "GF layer self check failed (S^-1 o S != id or M.M^-1 != I)");
+  // The device-built S-box must equal the host restatement of the same
+  // field arithmetic (gf.cuh is compiled for both sides).
+  for (int v = 0; v < 256; v++)
+    if (c->std_sbox[v] != sbox_forward((uint8_t)v) || c->std_inv[v] != sbox_inverse((uint8_t)v))
+      return fail(GAES_ETABLE, "device GF tables disagree with the host field arithmetic");
+  *out = c.get();
+  g_ctx[dev] = std::move(c);
+  return GAES_OK;
+}
+
+int current_ctx(DevCtx** out) {
+  int dev = 0;
+  if (device_count() <= 0) return fail(GAES_ENODEV, "no CUDA device visible");
+  GAES_CK(cudaGetDevice(&dev));
+  return get_ctx(dev, out);
+}
+
+// --------------------------------------------------------------------------
+// Round keys.
+inline uint32_t le32(const uint8_t* p) {
+  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+
+// out byte r of column = XOR_j lut[r][j][b_j]  (_kernel.pyx:44-47 applied to a key column)
+uint32_t mix_word_lut(uint32_t w, const uint8_t* lut) {
+  uint32_t o = 0;
+  for (int r = 0; r < 4; r++) {
+    uint8_t acc = 0;
+    for (int j = 0; j < 4; j++) acc ^= lut[(r * 4 + j) * 256 + ((w >> (8 * j)) & 0xFF)];
+    o |= (uint32_t)acc << (8 * r);
+  }
+  return o;
+}
+
+uint32_t inv_mix_word_std(uint32_t w) {
+  uint32_t o = 0;
+  for (int r = 0; r < 4; r++) {
+    uint8_t acc = 0;
+    for (int j = 0; j < 4; j++) acc ^= gf_mul(mix_coef(true, r, j), (uint8_t)(w >> (8 * j)));
+    o |= (uint32_t)acc << (8 * r);
+  }
+  return o;
+}
+
+// fold: XOR the shared IV into the first (encrypt) / last (decrypt) key.
+RoundKeys make_enc_keys(const uint8_t* rk, const uint8_t* iv, bool fold) {
+  RoundKeys k;
+  for (int i = 0; i < 44; i++) k.w[i] = le32(rk + 4 * i);
+  for (int c = 0; c < 4; c++) {
+    k.iv[c] = iv ? le32(iv + 4 * c) : 0u;
+    if (fold) k.w[c] ^= k.iv[c];
+  }
+  return k;
+}
+
+RoundKeys make_dec_keys(const uint8_t* rk, const uint8_t* iv, bool fold, const uint8_t* inv_lut) {
+  RoundKeys k;
+  for (int i = 0; i < 44; i++) {
+    const uint32_t w = le32(rk + 4 * i);
+    if (i >= 4 && i < 40)
+      k.w[i] = inv_lut ? mix_word_lut(w, inv_lut) : inv_mix_word_std(w);
+    else
+      k.w[i] = w;
+  }
+  for (int c = 0; c < 4; c++) {
+    k.iv[c] = iv ? le32(iv + 4 * c) : 0u;
+    if (fold) k.w[c] ^= k.iv[c];
+  }
+  return k;
+}
+
+// Each lut[r][j] row must be GF(2)-linear for the equivalent inverse cipher.
+bool lut_is_linear(const uint8_t* lut) {
+  for (int t = 0; t < 16; t++) {
+    const uint8_t* row = lut + t * 256;
+    if (row[0] != 0) return false;
+    for (int x = 1; x < 256; x++) {
+      uint8_t acc = 0;
+      for (int b = 0; b < 8; b++)
+        if (x & (1 << b)) acc ^= row[1 << b];
+      if (row[x] != acc) return false;
+    }
+  }
+  return true;
+}
+
+// Compact T tables for caller-supplied (box, lut), cached per device.
+int tables_for(DevCtx* c, const uint8_t* box, const uint8_t* lut, uint32_t** out) {
+  std::string key(reinterpret_cast<const char*>(box), 256);
+  key.append(reinterpret_cast<const char*>(lut), 4096);
+  std::lock_guard<std::mutex> lk(c->cache_mu);
+  auto it = c->cache.find(key);
+  if (it != c->cache.end()) {
+    *out = it->second;
+    return GAES_OK;
+  }
+  if (c->cache.size() >= 64) {  // bounded: drop everything (tables are cheap to rebuild)
+    GAES_CK(cudaDeviceSynchronize());
+    for (auto& kv : c->cache) cudaFree(kv.second);
+    c->cache.clear();
+  }
+  uint32_t* d = nullptr;
+  uint8_t* d_in = nullptr;
+  GAES_CK(cudaMalloc(&d, kCompactWords * 4));
+  GAES_CK(cudaMalloc(&d_in, 256 + 4096));
+  GAES_CK(cudaMemcpy(d_in, box, 256, cudaMemcpyHostToDevice));
+  GAES_CK(cudaMemcpy(d_in + 256, lut, 4096, cudaMemcpyHostToDevice));
+  GAES_CK(launch_build_tables(d_in, d_in + 256, d, 0));
+  note_kernel("k_build_tables");
+  GAES_CK(cudaDeviceSynchronize());
+  cudaFree(d_in);
+  c->cache.emplace(key, d);
+  *out = d;
+  return GAES_OK;
+}
+
+int ilp_default() {
+  static int ilp = std::max(1, std::min(2, env_int("GAES_ILP", 2)));
+  return ilp;
+}
+
+// --------------------------------------------------------------------------
+// Host-buffer pipeline.
+enum class Mode { kFolded, kChain, kEncRows, kGeneric };
+
+struct Job {
+  bool dec = false;
+  Mode mode = Mode::kFolded;
+  const uint8_t* data = nullptr;
+  const uint8_t* ivs = nullptr;  // per-row IVs (kChain with rows, kEncRows, kGeneric) or nullptr
+  uint8_t* out = nullptr;
+  size_t n = 0, m = 16;
+  RoundKeys rk;
+  const uint8_t* raw_rk = nullptr;  // generic path
+  const uint8_t *box = nullptr, *lut = nullptr, *perm = nullptr;
+  bool standard = true;  // use the device GF tables
+};
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+size_t chunk_bytes() {
+  static size_t b = (size_t)std::max(1, env_int("GAES_CHUNK_MB", 32)) << 20;
+  return b;
+}
+
+int ensure_slot(Slot& s, size_t bytes, size_t iv_bytes, bool staged_in, bool staged_out) {
+  if (s.cap < bytes) {
+    if (s.d_in) cudaFree(s.d_in);
+    if (s.d_out) cudaFree(s.d_out);
+    if (s.h_in) cudaFreeHost(s.h_in);
+    if (s.h_out) cudaFreeHost(s.h_out);
+    s.d_in = s.d_out = s.h_in = s.h_out = nullptr;
+    s.cap = 0;
+    GAES_CK(cudaMalloc(&s.d_in, bytes));
+    GAES_CK(cudaMalloc(&s.d_out, bytes));
+    s.cap = bytes;
+  }
+  if (staged_in && !s.h_in) GAES_CK(cudaMallocHost(&s.h_in, s.cap));
+  if (staged_out && !s.h_out) GAES_CK(cudaMallocHost(&s.h_out, s.cap));
+  if (iv_bytes && s.iv_cap < iv_bytes) {
+    if (s.d_iv) cudaFree(s.d_iv);
+    if (s.h_iv) cudaFreeHost(s.h_iv);
+    s.d_iv = s.h_iv = nullptr;
+    s.iv_cap = 0;
+    GAES_CK(cudaMalloc(&s.d_iv, iv_bytes));
+    GAES_CK(cudaMallocHost(&s.h_iv, iv_bytes));
+    s.iv_cap = iv_bytes;
+  }
+  return GAES_OK;
+}
+
+int finish_slot(Slot& s) {
+  GAES_CK(cudaEventSynchronize(s.done));
+  if (s.pending_dst) {
+    std::memcpy(s.pending_dst, s.h_out, s.pending_bytes);
+    s.pending_dst = nullptr;
+    s.pending_bytes = 0;
+  }
+  return GAES_OK;
+}
+
+int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t rows, const uint32_t* compact) {
+  const uint64_t bpr = j.m / 16;
+  const uint64_t nblk = rows * bpr;
+  switch (j.mode) {
+    case Mode::kFolded:
+      GAES_CK(launch_blocks(j.dec, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,
+                            c->sms, s.stream));
+      note_kernel(j.dec ? "k_blocks_dec_folded" : "k_blocks_enc_folded");
+      break;
+    case Mode::kChain:
+      GAES_CK(launch_blocks(j.dec, kIvChain, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk,
+                            j.ivs ? s.d_iv : nullptr, bpr, c->sms, s.stream));
+      note_kernel(j.dec ? "k_blocks_dec_chain" : "k_blocks_enc_chain");
+      break;
+    case Mode::kEncRows:
+      GAES_CK(launch_cbc_enc_rows(s.d_in, s.d_out, rows, bpr, compact, j.rk, j.ivs ? s.d_iv : nullptr, c->sms,
+                                  s.stream));
+      note_kernel("k_cbc_enc_rows");
+      break;
+    case Mode::kGeneric: {
+      uint8_t* sc = c->d_scratch;
+      GAES_CK(launch_generic(j.dec, s.d_in, s.d_iv, rows, j.m, sc + 256 + 4096 + 16, sc, sc + 256, sc + 256 + 4096,
+                             s.d_out, c->sms, s.stream));
+      note_kernel("k_generic_cbc");
+      break;
+    }
+  }
+  return GAES_OK;
+}
+
+// Runs rows [0, j.n) of `j` on device context c (one shard).
+int run_job(DevCtx* c, const Job& j) {
+  if (j.n == 0) return GAES_OK;
+  std::lock_guard<std::mutex> lk(c->mu);
+  int prev = 0;
+  GAES_CK(cudaGetDevice(&prev));
+  GAES_CK(cudaSetDevice(c->dev));
+  struct Restore {
+    int d;
+    ~Restore() { cudaSetDevice(d); }
+  } restore{prev};
+
+  const uint32_t* compact = nullptr;
+  if (j.mode != Mode::kGeneric) {
+    if (j.standard) {
+      compact = j.dec ? c->d_std_dec : c->d_std_enc;
+    } else {
+      uint32_t* t = nullptr;
+      int rc = tables_for(c, j.box, j.lut, &t);
+      if (rc) return rc;
+      compact = t;
+    }
+  } else {
+    uint8_t* sc = c->d_scratch;
+    GAES_CK(cudaMemcpy(sc, j.box, 256, cudaMemcpyHostToDevice));
+    GAES_CK(cudaMemcpy(sc + 256, j.lut, 4096, cudaMemcpyHostToDevice));
+    GAES_CK(cudaMemcpy(sc + 256 + 4096, j.perm, 16, cudaMemcpyHostToDevice));
+    GAES_CK(cudaMemcpy(sc + 256 + 4096 + 16, j.raw_rk, 176, cudaMemcpyHostToDevice));
+  }
+
+  const bool in_pinned = is_pinned(j.data);
+  const bool out_pinned = is_pinned(j.out);
+  const bool need_iv = j.ivs != nullptr;
+  const bool iv_pinned = need_iv && is_pinned(j.ivs);
+  size_t rows_per_chunk = std::max<size_t>(1, chunk_bytes() / j.m);
+  if (rows_per_chunk > j.n) rows_per_chunk = j.n;
+  const size_t nchunks = (j.n + rows_per_chunk - 1) / rows_per_chunk;
+  const int used_slots = (int)std::min<size_t>(kSlots, nchunks);
+  for (int k = 0; k < used_slots; k++) {
+    int rc = ensure_slot(c->slots[k], rows_per_chunk * j.m, need_iv ? rows_per_chunk * 16 : 0, !in_pinned,
+                         !out_pinned);
+    if (rc) return rc;
+  }
+  int rc_final = GAES_OK;
+  for (size_t ci = 0; ci < nchunks; ci++) {
+    Slot& s = c->slots[ci % kSlots];
+    if (ci >= (size_t)kSlots) {
+      int rc = finish_slot(s);
+      if (rc) return rc;
+    }
+    const size_t r0 = ci * rows_per_chunk;
+    const size_t rows = std::min(rows_per_chunk, j.n - r0);
+    const size_t off = r0 * j.m, bytes = rows * j.m;
+    const uint8_t* src = j.data + off;
+    if (!in_pinned) {
+      std::memcpy(s.h_in, src, bytes);
+      src = s.h_in;
+    }
+    GAES_CK(cudaMemcpyAsync(s.d_in, src, bytes, cudaMemcpyHostToDevice, s.stream));
+    if (need_iv) {
+      const uint8_t* ivsrc = j.ivs + r0 * 16;
+      if (!iv_pinned) {
+        std::memcpy(s.h_iv, ivsrc, rows * 16);
+        ivsrc = s.h_iv;
+      }
+      GAES_CK(cudaMemcpyAsync(s.d_iv, ivsrc, rows * 16, cudaMemcpyHostToDevice, s.stream));
+    }
+    int rc = launch_chunk(c, j, s, rows, compact);
+    if (rc) return rc;
+    if (out_pinned) {
+      GAES_CK(cudaMemcpyAsync(j.out + off, s.d_out, bytes, cudaMemcpyDeviceToHost, s.stream));
+    } else {
+      GAES_CK(cudaMemcpyAsync(s.h_out, s.d_out, bytes, cudaMemcpyDeviceToHost, s.stream));
+      s.pending_dst = j.out + off;
+      s.pending_bytes = bytes;
+    }
+    GAES_CK(cudaEventRecord(s.done, s.stream));
+  }
+  // drain in issue order
+  for (size_t ci = (nchunks > (size_t)kSlots ? nchunks - kSlots : 0); ci < nchunks; ci++) {
+    int rc = finish_slot(c->slots[ci % kSlots]);
+    if (rc && !rc_final) rc_final = rc;
+  }
+  return rc_final;
+}
+
+// parallel.py:37-50 applied to GPUs: contiguous, sizes differ by <= 1.
+std::vector<std::pair<size_t, size_t>> plan_rows(size_t n, int workers) {
+  std::vector<std::pair<size_t, size_t>> out;
+  const size_t used = std::min<size_t>((size_t)workers, n);
+  size_t start = 0;
+  for (size_t i = 0; i < used; i++) {
+    const size_t size = n / used + (i < n % used ? 1 : 0);
+    out.emplace_back(start, start + size);
+    start += size;
+  }
+  return out;
+}
+
+int gpus_in_use() {
+  const int n = device_count();
+  const int want = g_num_gpus.load();
+  if (want <= 0 || want > n) return n;
+  return want;
+}
+
+// Shard rows across devices; one host thread per device when > 1.
+int run_sharded(const Job& j) {
+  if (j.n == 0) return GAES_OK;
+  const int ndev = device_count();
+  if (ndev <= 0) return fail(GAES_ENODEV, "no CUDA device visible");
+  const int g = gpus_in_use();
+  auto chunks = plan_rows(j.n, g);
+  std::vector<DevCtx*> ctxs(chunks.size());
+  for (size_t i = 0; i < chunks.size(); i++) {
+    int rc = get_ctx((int)i, &ctxs[i]);
+    if (rc) return rc;
+  }
+  auto shard_job = [&](size_t i) {
+    Job s = j;
+    s.data = j.data + chunks[i].first * j.m;
+    s.out = j.out + chunks[i].first * j.m;
+    if (j.ivs) s.ivs = j.ivs + chunks[i].first * 16;
+    s.n = chunks[i].second - chunks[i].first;
+    return s;
+  };
+  if (chunks.size() == 1) return run_job(ctxs[0], shard_job(0));
+  std::vector<int> rcs(chunks.size(), GAES_OK);
+  std::vector<std::string> errs(chunks.size());
+  std::vector<std::thread> th;
+  for (size_t i = 0; i < chunks.size(); i++)
+    th.emplace_back([&, i] {
+      rcs[i] = run_job(ctxs[i], shard_job(i));
+      if (rcs[i]) errs[i] = t_err;
+    });
+  for (auto& t : th) t.join();
+  for (size_t i = 0; i < chunks.size(); i++)
+    if (rcs[i]) return fail(rcs[i], "gpu " + std::to_string(i) + ": " + errs[i]);
+  return GAES_OK;
+}
+
+bool rows_share_iv(const uint8_t* ivs, size_t n) {
+  for (size_t i = 1; i < n; i++)
+    if (std::memcmp(ivs, ivs + 16 * i, 16) != 0) return false;
+  return true;
+}
+
+int check_grid(const void* data, const void* out, size_t n, size_t m) {
+  if (n == 0) return GAES_OK;
+  if (!data || !out) return fail(GAES_EINVAL, "null data/out pointer");
+  if (m == 0 || m % 16 != 0) return fail(GAES_EINVAL, "padded width must be a positive multiple of 16");
+  return GAES_OK;
+}
+
+// The 7-argument backend contract (both directions).
+int cbc_host(bool dec, const uint8_t* data, const uint8_t* ivs, size_t n, size_t m, const uint8_t* rk,
+             const uint8_t* box, const uint8_t* lut, const uint8_t* perm, uint8_t* out) {
+  int rc = check_grid(data, out, n, m);
+  if (rc || n == 0) return rc;
+  if (!ivs || !rk || !box || !lut || !perm) return fail(GAES_EINVAL, "null table / IV pointer");
+  const uint8_t* std_perm = dec ? kInvShiftRowsSrc : kShiftRowsSrc;
+  const bool std_shift = std::memcmp(perm, std_perm, 16) == 0;
+  const bool linear = !dec || lut_is_linear(lut);
+  Job j;
+  j.dec = dec;
+  j.data = data;
+  j.out = out;
+  j.n = n;
+  j.m = m;
+  j.box = box;
+  j.lut = lut;
+  j.perm = perm;
+  j.raw_rk = rk;
+  j.standard = false;
+  if (!std_shift || !linear) {
+    j.mode = Mode::kGeneric;
+    j.ivs = ivs;
+    return run_sharded(j);
+  }
+  const size_t bpr = m / 16;
+  const bool shared = rows_share_iv(ivs, n);
+  if (bpr == 1 && shared) {
+    j.mode = Mode::kFolded;
+    j.rk = dec ? make_dec_keys(rk, ivs, true, lut) : make_enc_keys(rk, ivs, true);
+  } else if (dec || bpr == 1) {
+    j.mode = Mode::kChain;
+    j.ivs = shared ? nullptr : ivs;
+    j.rk = dec ? make_dec_keys(rk, ivs, false, lut) : make_enc_keys(rk, ivs, false);
+  } else {
+    j.mode = Mode::kEncRows;
+    j.ivs = shared ? nullptr : ivs;
+    j.rk = make_enc_keys(rk, ivs, false);
+  }
+  return run_sharded(j);
+}
+
+int shared_iv_host(bool dec, const uint8_t* data, size_t n, size_t m, const uint8_t* iv, const uint8_t* rk,
+                   uint8_t* out) {
+  int rc = check_grid(data, out, n, m);
+  if (rc || n == 0) return rc;
+  if (!rk) return fail(GAES_EINVAL, "null round keys");
+  static const uint8_t zero_iv[16] = {0};
+  if (!iv) iv = zero_iv;
+  Job j;
+  j.dec = dec;
+  j.data = data;
+  j.out = out;
+  j.n = n;
+  j.m = m;
+  j.standard = true;
+  const size_t bpr = m / 16;
+  if (bpr == 1) {
+    j.mode = Mode::kFolded;
+    j.rk = dec ? make_dec_keys(rk, iv, true, nullptr) : make_enc_keys(rk, iv, true);
+  } else if (dec) {
+    j.mode = Mode::kChain;
+    j.rk = make_dec_keys(rk, iv, false, nullptr);
+  } else {
+    j.mode = Mode::kEncRows;
+    j.rk = make_enc_keys(rk, iv, false);
+  }
+  return run_sharded(j);
+}
+
+}  // namespace
+
+// ==========================================================================
+// C ABI
+extern "C" {
+
+GAES_API int gaes_version(void) { return kVersion; }
+
+GAES_API const char* gaes_last_error(void) { return t_err.c_str(); }
+
+GAES_API int gaes_device_count(void) { return device_count(); }
+
+GAES_API int gaes_set_num_gpus(int n) {
+  g_num_gpus.store(n);
+  return gpus_in_use();
+}
+
+GAES_API int gaes_get_num_gpus(void) { return gpus_in_use(); }
+
+GAES_API uint64_t gaes_launch_count(void) { return g_launches.load(); }
+
+GAES_API const char* gaes_last_kernel(void) {
+  static thread_local std::string copy;
+  std::lock_guard<std::mutex> lk(g_name_mu);
+  copy = g_last_kernel;
+  return copy.c_str();
+}
+
+GAES_API int gaes_set_variant(int variant) {
+  if (variant != 0 && variant != 1) return fail(GAES_EINVAL, "variant not built (0 = auto, 1 = T-table)");
+  g_variant.store(variant);
+  return variant;
+}
+
+GAES_API int gaes_gf_tables(int device, uint8_t sbox[256], uint8_t inv_sbox[256], uint32_t te[1024],
+                            uint32_t td[1024]) {
+  DevCtx* c = nullptr;
+  int rc = get_ctx(device, &c);
+  if (rc) return rc;
+  if (sbox) std::memcpy(sbox, c->std_sbox, 256);
+  if (inv_sbox) std::memcpy(inv_sbox, c->std_inv, 256);
+  if (te) std::memcpy(te, c->std_te, sizeof(c->std_te));
+  if (td) std::memcpy(td, c->std_td, sizeof(c->std_td));
+  return GAES_OK;
+}
+
+GAES_API int gaes_tables_are_standard(const uint8_t sbox[256], const uint8_t mix_lut[4096],
+                                      const uint8_t shift_src[16], int decrypt) {
+  if (!sbox || !mix_lut || !shift_src) return fail(GAES_EINVAL, "null table pointer");
+  DevCtx* c = nullptr;
+  int rc = get_ctx(0, &c);
+  if (rc) return rc;
+  const uint8_t* box = decrypt ? c->std_inv : c->std_sbox;
+  if (std::memcmp(box, sbox, 256) != 0) return 0;
+  if (std::memcmp(shift_src, decrypt ? kInvShiftRowsSrc : kShiftRowsSrc, 16) != 0) return 0;
+  for (int r = 0; r < 4; r++)
+    for (int j = 0; j < 4; j++)
+      for (int x = 0; x < 256; x++)
+        if (mix_lut[(r * 4 + j) * 256 + x] != gf_mul(mix_coef(decrypt != 0, r, j), (uint8_t)x)) return 0;
+  return 1;
+}
+
+GAES_API int gaes_cbc_encrypt(const uint8_t* data, const uint8_t* ivs, size_t n, size_t m,
+                              const uint8_t round_keys[176], const uint8_t sbox[256], const uint8_t mix_lut[4096],
+                              const uint8_t shift_src[16], uint8_t* out) {
+  return cbc_host(false, data, ivs, n, m, round_keys, sbox, mix_lut, shift_src, out);
+}
+
+GAES_API int gaes_cbc_decrypt(const uint8_t* data, const uint8_t* ivs, size_t n, size_t m,
+                              const uint8_t round_keys[176], const uint8_t inv_sbox[256],
+                              const uint8_t inv_mix_lut[4096], const uint8_t inv_shift_src[16], uint8_t* out) {
+  return cbc_host(true, data, ivs, n, m, round_keys, inv_sbox, inv_mix_lut, inv_shift_src, out);
+}
+
+GAES_API int gaes_encrypt_shared_iv(const uint8_t* data, size_t n, size_t m, const uint8_t iv[16],
+                                    const uint8_t round_keys[176], uint8_t* out) {
+  return shared_iv_host(false, data, n, m, iv, round_keys, out);
+}
+
+GAES_API int gaes_decrypt_shared_iv(const uint8_t* data, size_t n, size_t m, const uint8_t iv[16],
+                                    const uint8_t round_keys[176], uint8_t* out) {
+  return shared_iv_host(true, data, n, m, iv, round_keys, out);
+}
+
+GAES_API int gaes_encrypt_blocks_dev(const void* in, void* out, size_t n_blocks, const uint8_t round_keys[176],
+                                     const uint8_t iv[16], void* stream) {
+  if (n_blocks == 0) return GAES_OK;
+  if (!in || !out || !round_keys) return fail(GAES_EINVAL, "null pointer");
+  DevCtx* c = nullptr;
+  int rc = current_ctx(&c);
+  if (rc) return rc;
+  const RoundKeys k = make_enc_keys(round_keys, iv, true);
+  GAES_CK(launch_blocks(false, kIvFolded, ilp_default(), in, out, n_blocks, c->d_std_enc, k, nullptr, 1, c->sms,
+                        (cudaStream_t)stream));
+  note_kernel("k_blocks_enc_folded");
+  return GAES_OK;
+}
+
+GAES_API int gaes_decrypt_blocks_dev(const void* in, void* out, size_t n_blocks, const uint8_t round_keys[176],
+                                     const uint8_t iv[16], void* stream) {
+  if (n_blocks == 0) return GAES_OK;
+  if (!in || !out || !round_keys) return fail(GAES_EINVAL, "null pointer");
+  DevCtx* c = nullptr;
+  int rc = current_ctx(&c);
+  if (rc) return rc;
+  const RoundKeys k = make_dec_keys(round_keys, iv, true, nullptr);
+  GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), in, out, n_blocks, c->d_std_dec, k, nullptr, 1, c->sms,
+                        (cudaStream_t)stream));
+  note_kernel("k_blocks_dec_folded");
+  return GAES_OK;
+}
+
+GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m, const void* ivs_dev,
+                                  const uint8_t iv[16], const uint8_t round_keys[176], void* stream) {
+  int rc = check_grid(in, out, n, m);
+  if (rc || n == 0) return rc;
+  if (!round_keys) return fail(GAES_EINVAL, "null round keys");
+  DevCtx* c = nullptr;
+  rc = current_ctx(&c);
+  if (rc) return rc;
+  const uint64_t bpr = m / 16;
+  if (bpr == 1 && !ivs_dev) return gaes_encrypt_blocks_dev(in, out, n, round_keys, iv, stream);
+  const RoundKeys k = make_enc_keys(round_keys, iv, false);
+  if (bpr == 1) {
+    GAES_CK(launch_blocks(false, kIvChain, ilp_default(), in, out, n, c->d_std_enc, k, ivs_dev, 1, c->sms,
+                          (cudaStream_t)stream));
+    note_kernel("k_blocks_enc_chain");
+  } else {
+    GAES_CK(launch_cbc_enc_rows(in, out, n, bpr, c->d_std_enc, k, ivs_dev, c->sms, (cudaStream_t)stream));
+    note_kernel("k_cbc_enc_rows");
+  }
+  return GAES_OK;
+}
+
+GAES_API int gaes_cbc_decrypt_dev(const void* in, void* out, size_t n, size_t m, const void* ivs_dev,
+                                  const uint8_t iv[16], const uint8_t round_keys[176], void* stream) {
+  int rc = check_grid(in, out, n, m);
+  if (rc || n == 0) return rc;
+  if (!round_keys) return fail(GAES_EINVAL, "null round keys");
+  DevCtx* c = nullptr;
+  rc = current_ctx(&c);
+  if (rc) return rc;
+  const uint64_t bpr = m / 16;
+  if (bpr == 1 && !ivs_dev) return gaes_decrypt_blocks_dev(in, out, n, round_keys, iv, stream);
+  const RoundKeys k = make_dec_keys(round_keys, iv, false, nullptr);
+  GAES_CK(launch_blocks(true, kIvChain, ilp_default(), in, out, n * bpr, c->d_std_dec, k, ivs_dev, bpr, c->sms,
+                        (cudaStream_t)stream));
+  note_kernel("k_blocks_dec_chain");
+  return GAES_OK;
+}
+
+GAES_API int gaes_expand_keys_dev(const void* keys, size_t k, void* rk_enc, void* rk_dec, void* stream) {
+  if (k == 0) return GAES_OK;
+  if (!keys || !rk_enc) return fail(GAES_EINVAL, "null pointer");
+  DevCtx* c = nullptr;
+  int rc = current_ctx(&c);
+  if (rc) return rc;
+  GAES_CK(launch_expand_keys((const uint8_t*)keys, k, c->d_std_enc, (uint8_t*)rk_enc, (uint8_t*)rk_dec,
+                             (cudaStream_t)stream));
+  note_kernel("k_expand_keys");
+  return GAES_OK;
+}
+
+GAES_API int gaes_many_key_encrypt_dev(const void* in, void* out, size_t blocks_per_key, size_t k,
+                                       const void* rk_enc, const void* ivs_dev, void* stream) {
+  if (k == 0 || blocks_per_key == 0) return GAES_OK;
+  if (!in || !out || !rk_enc) return fail(GAES_EINVAL, "null pointer");
+  DevCtx* c = nullptr;
+  int rc = current_ctx(&c);
+  if (rc) return rc;
+  GAES_CK(launch_many_key(false, in, out, blocks_per_key, k, c->d_std_enc, rk_enc, ivs_dev, c->sms,
+                          (cudaStream_t)stream));
+  note_kernel("k_many_key_enc");
+  return GAES_OK;
+}
+
+GAES_API int gaes_many_key_decrypt_dev(const void* in, void* out, size_t blocks_per_key, size_t k,
+                                       const void* rk_dec, const void* ivs_dev, void* stream) {
+  if (k == 0 || blocks_per_key == 0) return GAES_OK;
+  if (!in || !out || !rk_dec) return fail(GAES_EINVAL, "null pointer");
+  DevCtx* c = nullptr;
+  int rc = current_ctx(&c);
+  if (rc) return rc;
+  GAES_CK(launch_many_key(true, in, out, blocks_per_key, k, c->d_std_dec, rk_dec, ivs_dev, c->sms,
+                          (cudaStream_t)stream));
+  note_kernel("k_many_key_dec");
+  return GAES_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,422 @@
+// kernels.cu -- sm_100a kernels of the AES-128 hot path.
+//
+//   k_gf_build        GF(2^8) layer: S, S^-1, Te, Td from field arithmetic
+//   k_build_tables    T tables from the tables the reference hands over
+//   k_blocks          M = 16 blocks (and block-parallel CBC decrypt), T-table
+//   k_cbc_enc_rows    CBC encrypt along rows (serial chain, M > 16)
+//   k_generic_cbc     byte-level round for arbitrary shift permutations /
+//                     non-linear mix tables (correctness path, still GPU)
+//   k_expand_keys     batched key schedule (key_schedule.py:50-70)
+//   k_many_key        many-key batch (config 5)
+//
+// Reference semantics: pkg/src/gaes/_kernel.pyx:12-101.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "aes_ttable.cuh"
+#include "gf.cuh"
+#include "kernels.h"
+
+namespace gaes {
+
+// ---------------------------------------------------------------------------
+// GF layer: one CTA of 256 threads, thread v owns table entry v.
+// out_enc / out_dec: compact 5 x 256 words each; sbox/inv: 256 bytes each.
+// err: set to nonzero if the cross checks of sbox_gen.py:66-79 (S^-1(S(v)) == v)
+// or aes_cbc.py:126-132 (M . M^-1 == I) fail.
+__global__ void k_gf_build(uint32_t* __restrict__ out_enc, uint32_t* __restrict__ out_dec,
+                           uint8_t* __restrict__ sbox_out, uint8_t* __restrict__ inv_out, int* __restrict__ err) {
+  __shared__ uint8_t S[256], Si[256];
+  const int v = threadIdx.x;
+  S[v] = sbox_forward((uint8_t)v);
+  Si[v] = sbox_inverse((uint8_t)v);
+  __syncthreads();
+  if (Si[S[v]] != v) atomicOr(err, 1);
+  if (v < 16) {  // (M . M^-1)[r][c] == delta(r, c)
+    const int r = v >> 2, c = v & 3;
+    uint8_t acc = 0;
+    for (int k = 0; k < 4; k++) acc ^= gf_mul(mix_coef(false, r, k), mix_coef(true, k, c));
+    if (acc != (r == c ? 1 : 0)) atomicOr(err, 2);
+  }
+  for (int j = 0; j < 4; j++) {
+    uint32_t te = 0, td = 0;
+    for (int r = 0; r < 4; r++) {
+      te |= (uint32_t)gf_mul(mix_coef(false, r, j), S[v]) << (8 * r);
+      td |= (uint32_t)gf_mul(mix_coef(true, r, j), Si[v]) << (8 * r);
+    }
+    out_enc[j * 256 + v] = te;
+    out_dec[j * 256 + v] = td;
+  }
+  out_enc[4 * 256 + v] = S[v];
+  out_dec[4 * 256 + v] = Si[v];
+  sbox_out[v] = S[v];
+  inv_out[v] = Si[v];
+}
+
+// T tables from caller-supplied tables: T_j[x] = pack_r lut[r][j][box[x]].
+__global__ void k_build_tables(const uint8_t* __restrict__ box, const uint8_t* __restrict__ lut,
+                               uint32_t* __restrict__ out) {
+  const int x = threadIdx.x;
+  const uint8_t s = box[x];
+  for (int j = 0; j < 4; j++) {
+    uint32_t t = 0;
+    for (int r = 0; r < 4; r++) t |= (uint32_t)lut[(r * 4 + j) * 256 + s] << (8 * r);
+    out[j * 256 + x] = t;
+  }
+  out[4 * 256 + x] = s;
+}
+
+// ---------------------------------------------------------------------------
+// Streaming 16-byte loads/stores (data is touched exactly once).
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(uint4* p, uint4 v) { __stcs(p, v); }
+
+// M = 16 blocks and block-parallel CBC decrypt.
+//   IVM == kIvFolded: IV already folded into rk (encrypt: rk0 ^= iv;
+//                     decrypt: final key rk0 ^= iv); rows are single blocks.
+//   IVM == kIvChain : chain value x for block b of row i = b / bpr, j = b % bpr:
+//                     x = j ? in[b-1] : (ivs ? ivs[i] : rk.iv).
+//                     encrypt: state ^= x (only valid for bpr == 1);
+//                     decrypt: out ^= x.
+template <int ILP, bool DEC, int IVM>
+__global__ void __launch_bounds__(kBlockThreads, 1)
+    k_blocks(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks,
+             const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
+             const uint4* __restrict__ ivs, uint64_t bpr) {
+  extern __shared__ __align__(1024) char smem[];
+  fill_tables(smem, compact);
+  const uint32_t lb = (threadIdx.x & 31) * 4;
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+
+  uint4 cur[ILP];
+#pragma unroll
+  for (int k = 0; k < ILP; k++)
+    if (b + k * T < n_blocks) cur[k] = ld_stream(in + b + k * T);
+
+  while (b < n_blocks) {
+    const uint64_t nb = b + ILP * T;
+    uint4 nxt[ILP];
+#pragma unroll
+    for (int k = 0; k < ILP; k++)
+      if (nb + k * T < n_blocks) nxt[k] = ld_stream(in + nb + k * T);
+
+#pragma unroll
+    for (int k = 0; k < ILP; k++) {
+      const uint64_t bk = b + k * T;
+      if (bk < n_blocks) {
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (IVM == kIvChain) {
+          uint64_t j = 0, row = bk;
+          if (bpr != 1) { row = bk / bpr; j = bk - row * bpr; }
+          if (j) x = __ldg(in + bk - 1);
+          else if (ivs) x = __ldg(ivs + row);
+          else x = make_uint4(rk.iv[0], rk.iv[1], rk.iv[2], rk.iv[3]);
+        }
+        uint32_t s0 = cur[k].x, s1 = cur[k].y, s2 = cur[k].z, s3 = cur[k].w;
+        if (!DEC) {
+          s0 ^= rk.w[0] ^ x.x; s1 ^= rk.w[1] ^ x.y; s2 ^= rk.w[2] ^ x.z; s3 ^= rk.w[3] ^ x.w;
+          encrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
+        } else {
+          s0 ^= rk.w[40]; s1 ^= rk.w[41]; s2 ^= rk.w[42]; s3 ^= rk.w[43];
+          decrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
+          s0 ^= rk.w[0] ^ x.x; s1 ^= rk.w[1] ^ x.y; s2 ^= rk.w[2] ^ x.z; s3 ^= rk.w[3] ^ x.w;
+        }
+        st_stream(out + bk, make_uint4(s0, s1, s2, s3));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < ILP; k++) cur[k] = nxt[k];
+    b = nb;
+  }
+}
+
+// CBC encrypt along rows: thread per row, serial chain (_kernel.pyx:29-54).
+__global__ void __launch_bounds__(kBlockThreads, 1)
+    k_cbc_enc_rows(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_rows, uint64_t bpr,
+                   const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
+                   const uint4* __restrict__ ivs) {
+  extern __shared__ __align__(1024) char smem[];
+  fill_tables(smem, compact);
+  const uint32_t lb = (threadIdx.x & 31) * 4;
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t row = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n_rows; row += T) {
+    uint4 c = ivs ? __ldg(ivs + row) : make_uint4(rk.iv[0], rk.iv[1], rk.iv[2], rk.iv[3]);
+    const uint4* src = in + row * bpr;
+    uint4* dst = out + row * bpr;
+    uint4 p = ld_stream(src);
+    for (uint64_t j = 0; j < bpr; j++) {
+      const uint4 pn = (j + 1 < bpr) ? ld_stream(src + j + 1) : p;
+      uint32_t s0 = p.x ^ c.x ^ rk.w[0], s1 = p.y ^ c.y ^ rk.w[1];
+      uint32_t s2 = p.z ^ c.z ^ rk.w[2], s3 = p.w ^ c.w ^ rk.w[3];
+      encrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
+      c = make_uint4(s0, s1, s2, s3);
+      st_stream(dst + j, c);
+      p = pn;
+    }
+  }
+}
+
+// Byte-level CBC with arbitrary tables: a direct transcription of
+// _kernel.pyx:12-101 (thread per row).  Used only when the tables handed
+// over are outside what the T-table kernels can express.
+template <bool DEC>
+__global__ void k_generic_cbc(const uint8_t* __restrict__ data, const uint8_t* __restrict__ ivs, uint64_t n,
+                              uint64_t m, const uint8_t* __restrict__ rk, const uint8_t* __restrict__ box,
+                              const uint8_t* __restrict__ lut, const uint8_t* __restrict__ perm,
+                              uint8_t* __restrict__ out) {
+  __shared__ uint8_t sbox[256], mix[4096], shift[16], keys[176];
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) mix[i] = lut[i];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) sbox[i] = box[i];
+  for (int i = threadIdx.x; i < 176; i += blockDim.x) keys[i] = rk[i];
+  if (threadIdx.x < 16) shift[threadIdx.x] = perm[threadIdx.x];
+  __syncthreads();
+  const uint64_t nblocks = m / 16;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint8_t state[16], tmp[16], chain[16];
+    for (int j = 0; j < 16; j++) chain[j] = ivs[i * 16 + j];
+    for (uint64_t blk = 0; blk < nblocks; blk++) {
+      const uint8_t* src = data + i * m + 16 * blk;
+      uint8_t* dst = out + i * m + 16 * blk;
+      if (!DEC) {
+        for (int j = 0; j < 16; j++) state[j] = src[j] ^ chain[j] ^ keys[j];
+        for (int r = 1; r <= 10; r++) {
+          for (int j = 0; j < 16; j++) tmp[j] = sbox[state[j]];
+          for (int j = 0; j < 16; j++) state[j] = tmp[shift[j]];
+          if (r < 10) {
+            for (int c = 0; c < 16; c += 4)
+              for (int j = 0; j < 4; j++)
+                tmp[c + j] = mix[(j * 4 + 0) * 256 + state[c]] ^ mix[(j * 4 + 1) * 256 + state[c + 1]] ^
+                             mix[(j * 4 + 2) * 256 + state[c + 2]] ^ mix[(j * 4 + 3) * 256 + state[c + 3]];
+            for (int j = 0; j < 16; j++) state[j] = tmp[j];
+          }
+          for (int j = 0; j < 16; j++) state[j] ^= keys[16 * r + j];
+        }
+        for (int j = 0; j < 16; j++) { dst[j] = state[j]; chain[j] = state[j]; }
+      } else {
+        for (int j = 0; j < 16; j++) state[j] = src[j];
+        for (int r = 10; r >= 1; r--) {
+          for (int j = 0; j < 16; j++) state[j] ^= keys[16 * r + j];
+          if (r < 10) {
+            for (int c = 0; c < 16; c += 4)
+              for (int j = 0; j < 4; j++)
+                tmp[c + j] = mix[(j * 4 + 0) * 256 + state[c]] ^ mix[(j * 4 + 1) * 256 + state[c + 1]] ^
+                             mix[(j * 4 + 2) * 256 + state[c + 2]] ^ mix[(j * 4 + 3) * 256 + state[c + 3]];
+            for (int j = 0; j < 16; j++) state[j] = tmp[j];
+          }
+          for (int j = 0; j < 16; j++) tmp[j] = state[shift[j]];
+          for (int j = 0; j < 16; j++) state[j] = sbox[tmp[j]];
+        }
+        for (int j = 0; j < 16; j++) dst[j] = state[j] ^ keys[j] ^ chain[j];
+        for (int j = 0; j < 16; j++) chain[j] = src[j];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Batched key schedule: thread per key.  key_schedule.py:50-70; rcon =
+// x^(r-1) (key_schedule.py:41-43) by repeated xtime.  rk_dec rows 1..9 are
+// InvMixColumns of the encryption rows (equivalent inverse cipher).
+__device__ __forceinline__ uint32_t inv_mix_word(uint32_t w) {
+  uint32_t o = 0;
+#pragma unroll
+  for (int r = 0; r < 4; r++) {
+    uint8_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc ^= gf_mul(mix_coef(true, r, j), (uint8_t)(w >> (8 * j)));
+    o |= (uint32_t)acc << (8 * r);
+  }
+  return o;
+}
+
+__global__ void k_expand_keys(const uint8_t* __restrict__ keys, uint64_t k, const uint32_t* __restrict__ compact_enc,
+                              uint8_t* __restrict__ rk_enc, uint8_t* __restrict__ rk_dec) {
+  __shared__ uint8_t S[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) S[i] = (uint8_t)compact_enc[4 * 256 + i];
+  __syncthreads();
+  const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= k) return;
+  uint32_t w[44];
+  const uint8_t* key = keys + id * 16;
+#pragma unroll
+  for (int c = 0; c < 4; c++)
+    w[c] = (uint32_t)key[4 * c] | ((uint32_t)key[4 * c + 1] << 8) | ((uint32_t)key[4 * c + 2] << 16) |
+           ((uint32_t)key[4 * c + 3] << 24);
+  uint8_t rcon = 1;
+#pragma unroll
+  for (int r = 1; r <= 10; r++) {
+    const uint32_t p = w[4 * r - 1];
+    // RotWord (prev[13:16] + prev[12:13]) then SubWord, rcon into byte 0
+    uint32_t t = (uint32_t)S[(p >> 8) & 0xFF] | ((uint32_t)S[(p >> 16) & 0xFF] << 8) |
+                 ((uint32_t)S[(p >> 24) & 0xFF] << 16) | ((uint32_t)S[p & 0xFF] << 24);
+    t ^= rcon;
+    w[4 * r + 0] = w[4 * r - 4] ^ t;
+    w[4 * r + 1] = w[4 * r - 3] ^ w[4 * r + 0];
+    w[4 * r + 2] = w[4 * r - 2] ^ w[4 * r + 1];
+    w[4 * r + 3] = w[4 * r - 1] ^ w[4 * r + 2];
+    rcon = (uint8_t)((rcon << 1) ^ ((rcon & 0x80) ? 0x1B : 0));
+  }
+  uint32_t* oe = reinterpret_cast<uint32_t*>(rk_enc + id * 176);
+#pragma unroll
+  for (int i = 0; i < 44; i++) oe[i] = w[i];
+  if (rk_dec) {
+    uint32_t* od = reinterpret_cast<uint32_t*>(rk_dec + id * 176);
+#pragma unroll
+    for (int i = 0; i < 44; i++) od[i] = (i >= 4 && i < 40) ? inv_mix_word(w[i]) : w[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Many-key batch: key i owns blocks [i*bpk, (i+1)*bpk).  Round keys live in
+// registers and are reloaded only when a thread's grid-stride walk crosses
+// into the next key's range.
+template <bool DEC>
+__global__ void __launch_bounds__(kManyKeyThreads, 1)
+    k_many_key(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t bpk, uint64_t n_keys,
+               const uint32_t* __restrict__ compact, const uint4* __restrict__ rks, const uint4* __restrict__ ivs) {
+  extern __shared__ __align__(1024) char smem[];
+  fill_tables(smem, compact);
+  const uint32_t lb = (threadIdx.x & 31) * 4;
+  const uint64_t n_blocks = bpk * n_keys;
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n_blocks) return;
+  uint64_t key = b / bpk;
+  uint64_t key_end = (key + 1) * bpk;
+  RoundKeys rk;
+  auto load_key = [&](uint64_t kid) {
+#pragma unroll
+    for (int q = 0; q < 11; q++) {
+      const uint4 v = __ldg(rks + kid * 11 + q);
+      rk.w[4 * q + 0] = v.x; rk.w[4 * q + 1] = v.y; rk.w[4 * q + 2] = v.z; rk.w[4 * q + 3] = v.w;
+    }
+    const uint4 iv = ivs ? __ldg(ivs + kid) : make_uint4(0, 0, 0, 0);
+    rk.w[0] ^= iv.x; rk.w[1] ^= iv.y; rk.w[2] ^= iv.z; rk.w[3] ^= iv.w;
+  };
+  load_key(key);
+  uint4 cur = ld_stream(in + b);
+  while (b < n_blocks) {
+    const uint64_t nb = b + T;
+    uint4 nxt = cur;
+    if (nb < n_blocks) nxt = ld_stream(in + nb);
+    if (b >= key_end) {
+      key = b / bpk;
+      key_end = (key + 1) * bpk;
+      load_key(key);
+    }
+    uint32_t s0 = cur.x, s1 = cur.y, s2 = cur.z, s3 = cur.w;
+    if (!DEC) {
+      s0 ^= rk.w[0]; s1 ^= rk.w[1]; s2 ^= rk.w[2]; s3 ^= rk.w[3];
+      encrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
+    } else {
+      s0 ^= rk.w[40]; s1 ^= rk.w[41]; s2 ^= rk.w[42]; s3 ^= rk.w[43];
+      decrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
+      s0 ^= rk.w[0]; s1 ^= rk.w[1]; s2 ^= rk.w[2]; s3 ^= rk.w[3];
+    }
+    st_stream(out + b, make_uint4(s0, s1, s2, s3));
+    cur = nxt;
+    b = nb;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers.
+
+static int grid_for(uint64_t work_items, int per_thread, int sms, int cta_threads = kBlockThreads) {
+  const uint64_t threads = (work_items + per_thread - 1) / per_thread;
+  uint64_t ctas = (threads + cta_threads - 1) / cta_threads;
+  if (ctas > (uint64_t)sms) ctas = sms;
+  if (ctas < 1) ctas = 1;
+  return (int)ctas;
+}
+
+template <typename K>
+static cudaError_t set_smem(K kernel) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+}
+
+cudaError_t launch_gf_build(uint32_t* enc, uint32_t* dec, uint8_t* sbox, uint8_t* inv, int* err, cudaStream_t s) {
+  k_gf_build<<<1, 256, 0, s>>>(enc, dec, sbox, inv, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_tables(const uint8_t* box, const uint8_t* lut, uint32_t* out, cudaStream_t s) {
+  k_build_tables<<<1, 256, 0, s>>>(box, lut, out);
+  return cudaGetLastError();
+}
+
+template <int ILP, bool DEC, int IVM>
+static cudaError_t launch_blocks_t(const void* in, void* out, uint64_t n, const uint32_t* compact,
+                                   const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms, cudaStream_t s) {
+  auto kern = k_blocks<ILP, DEC, IVM>;
+  cudaError_t e = set_smem(kern);
+  if (e != cudaSuccess) return e;
+  const int grid = grid_for(n, ILP, sms);
+  kern<<<grid, kBlockThreads, kSmemBytes, s>>>((const uint4*)in, (uint4*)out, n, compact, rk, (const uint4*)ivs,
+                                               bpr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* out, uint64_t n_blocks,
+                          const uint32_t* compact, const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms,
+                          cudaStream_t s) {
+  if (n_blocks == 0) return cudaSuccess;
+#define GAES_CASE(I, D, M) \
+  if (ilp == I && dec == D && ivmode == M) return launch_blocks_t<I, D, M>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s);
+  GAES_CASE(1, false, kIvFolded) GAES_CASE(1, true, kIvFolded) GAES_CASE(1, false, kIvChain)
+  GAES_CASE(1, true, kIvChain) GAES_CASE(2, false, kIvFolded) GAES_CASE(2, true, kIvFolded)
+  GAES_CASE(2, false, kIvChain) GAES_CASE(2, true, kIvChain)
+#undef GAES_CASE
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint64_t bpr, const uint32_t* compact,
+                                const RoundKeys& rk, const void* ivs, int sms, cudaStream_t s) {
+  if (n_rows == 0) return cudaSuccess;
+  cudaError_t e = set_smem(k_cbc_enc_rows);
+  if (e != cudaSuccess) return e;
+  const int grid = grid_for(n_rows, 1, sms);
+  k_cbc_enc_rows<<<grid, kBlockThreads, kSmemBytes, s>>>((const uint4*)in, (uint4*)out, n_rows, bpr, compact, rk,
+                                                         (const uint4*)ivs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_generic(bool dec, const uint8_t* data, const uint8_t* ivs, uint64_t n, uint64_t m,
+                           const uint8_t* rk, const uint8_t* box, const uint8_t* lut, const uint8_t* perm,
+                           uint8_t* out, int sms, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  uint64_t ctas = (n + 127) / 128;
+  if (ctas > (uint64_t)sms * 8) ctas = (uint64_t)sms * 8;
+  if (dec)
+    k_generic_cbc<true><<<(int)ctas, 128, 0, s>>>(data, ivs, n, m, rk, box, lut, perm, out);
+  else
+    k_generic_cbc<false><<<(int)ctas, 128, 0, s>>>(data, ivs, n, m, rk, box, lut, perm, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand_keys(const uint8_t* keys, uint64_t k, const uint32_t* compact_enc, uint8_t* rk_enc,
+                               uint8_t* rk_dec, cudaStream_t s) {
+  if (k == 0) return cudaSuccess;
+  const int threads = 128;
+  const uint64_t ctas = (k + threads - 1) / threads;
+  k_expand_keys<<<(unsigned)ctas, threads, 0, s>>>(keys, k, compact_enc, rk_enc, rk_dec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_many_key(bool dec, const void* in, void* out, uint64_t bpk, uint64_t n_keys,
+                            const uint32_t* compact, const void* rks, const void* ivs, int sms, cudaStream_t s) {
+  if (bpk == 0 || n_keys == 0) return cudaSuccess;
+  cudaError_t e = dec ? set_smem(k_many_key<true>) : set_smem(k_many_key<false>);
+  if (e != cudaSuccess) return e;
+  const int grid = grid_for(bpk * n_keys, 1, sms, kManyKeyThreads);
+  if (dec)
+    k_many_key<true><<<grid, kManyKeyThreads, kSmemBytes, s>>>((const uint4*)in, (uint4*)out, bpk, n_keys, compact,
+                                                             (const uint4*)rks, (const uint4*)ivs);
+  else
+    k_many_key<false><<<grid, kManyKeyThreads, kSmemBytes, s>>>((const uint4*)in, (uint4*)out, bpk, n_keys, compact,
+                                                              (const uint4*)rks, (const uint4*)ivs);
+  return cudaGetLastError();
+}
+
+}  // namespace gaes

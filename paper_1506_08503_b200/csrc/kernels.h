@@ -1,0 +1,31 @@
+// kernels.h -- internal (C++) launch interface between the kernels and the
+// host dispatcher.  Not part of the C ABI (see include/gaes_b200.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "types.h"
+
+namespace gaes {
+
+static constexpr int kBlockThreads = 1024;     // k_blocks / k_cbc_enc_rows: 1 CTA per SM
+static constexpr int kManyKeyThreads = 512;    // k_many_key: 44 round-key registers per thread
+static constexpr int kIvFolded = 0;
+static constexpr int kIvChain = 1;
+
+cudaError_t launch_gf_build(uint32_t* enc, uint32_t* dec, uint8_t* sbox, uint8_t* inv, int* err, cudaStream_t s);
+cudaError_t launch_build_tables(const uint8_t* box, const uint8_t* lut, uint32_t* out, cudaStream_t s);
+cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* out, uint64_t n_blocks,
+                          const uint32_t* compact, const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms,
+                          cudaStream_t s);
+cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint64_t bpr, const uint32_t* compact,
+                                const RoundKeys& rk, const void* ivs, int sms, cudaStream_t s);
+cudaError_t launch_generic(bool dec, const uint8_t* data, const uint8_t* ivs, uint64_t n, uint64_t m,
+                           const uint8_t* rk, const uint8_t* box, const uint8_t* lut, const uint8_t* perm,
+                           uint8_t* out, int sms, cudaStream_t s);
+cudaError_t launch_expand_keys(const uint8_t* keys, uint64_t k, const uint32_t* compact_enc, uint8_t* rk_enc,
+                               uint8_t* rk_dec, cudaStream_t s);
+cudaError_t launch_many_key(bool dec, const void* in, void* out, uint64_t bpk, uint64_t n_keys,
+                            const uint32_t* compact, const void* rks, const void* ivs, int sms, cudaStream_t s);
+
+}  // namespace gaes

@@ -1,0 +1,188 @@
+"""Device-resident API over torch CUDA tensors (stream-ordered, no host sync).
+
+These are the calls a GPU-native user makes with data already in HBM; the
+bench's ``value`` (kernel throughput) is measured through them.  All take
+uint8 CUDA tensors laid out like the reference's grids (row = message,
+16-byte block = AES state in FIPS-197 byte order, aes_cbc.py:3-5) and run
+on ``torch.cuda.current_stream()``.
+
+* ``encrypt_blocks`` / ``decrypt_blocks``: the north-star M = 16 path,
+  C_i = E_K(P_i ^ IV), P_i = D_K(C_i) ^ IV (shared IV folded into the key).
+* ``cbc_encrypt`` / ``cbc_decrypt``: general N x M grids, shared or
+  per-message IVs (_kernel.pyx:12-101 semantics).
+* ``expand_keys``: batched GPU key schedule (key_schedule.py:50-70).
+* ``many_key_encrypt`` / ``many_key_decrypt``: config-5 many-key batches.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _u8_cuda(t: torch.Tensor, name: str, ndim: int | None = None) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.uint8:
+        raise ValueError(f"{name} must be uint8, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if ndim is not None and t.dim() != ndim:
+        raise ValueError(f"{name} must be {ndim}-D")
+    return t
+
+
+def _host_bytes(x, n: int, name: str) -> np.ndarray | None:
+    if x is None:
+        return None
+    if isinstance(x, torch.Tensor):
+        x = x.detach().cpu().numpy()
+    a = np.ascontiguousarray(np.frombuffer(bytes(x), np.uint8) if isinstance(x, (bytes, bytearray))
+                             else np.asarray(x, np.uint8)).reshape(-1)
+    if a.size != n:
+        raise ValueError(f"{name} must be {n} bytes")
+    return a
+
+
+def _p(a) -> int | None:
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.__array_interface__["data"][0]
+    return a.data_ptr()
+
+
+def _check_grid(x: torch.Tensor, out: torch.Tensor | None):
+    x = _u8_cuda(x, "input", 2)
+    if x.shape[1] == 0 or x.shape[1] % 16:
+        raise ValueError("padded width must be a positive multiple of 16")
+    if out is None:
+        out = torch.empty_like(x)
+    out = _u8_cuda(out, "out", 2)
+    if out.shape != x.shape or out.device != x.device:
+        raise ValueError("out must match input shape and device")
+    return x, out
+
+
+def encrypt_blocks(x: torch.Tensor, round_keys, iv=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """M = 16 rows: out_i = E_K(x_i ^ iv). round_keys: u8[11,16] (gen_keys)."""
+    x, out = _check_grid(x, out)
+    if x.shape[1] != 16:
+        raise ValueError("encrypt_blocks takes N x 16 rows; use cbc_encrypt for wider rows")
+    rk = _host_bytes(round_keys, 176, "round_keys")
+    ivb = _host_bytes(iv, 16, "iv")
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.lib().gaes_encrypt_blocks_dev(_p(x), _p(out), x.shape[0], _p(rk), _p(ivb), _stream()))
+    return out
+
+
+def decrypt_blocks(x: torch.Tensor, round_keys, iv=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    x, out = _check_grid(x, out)
+    if x.shape[1] != 16:
+        raise ValueError("decrypt_blocks takes N x 16 rows; use cbc_decrypt for wider rows")
+    rk = _host_bytes(round_keys, 176, "round_keys")
+    ivb = _host_bytes(iv, 16, "iv")
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.lib().gaes_decrypt_blocks_dev(_p(x), _p(out), x.shape[0], _p(rk), _p(ivb), _stream()))
+    return out
+
+
+def _ivs(ivs, n: int, device):
+    """(device tensor N x 16 or None, host shared IV or None)."""
+    if ivs is None:
+        return None, None
+    if isinstance(ivs, torch.Tensor) and ivs.is_cuda:
+        ivs = _u8_cuda(ivs, "ivs", 2)
+        if tuple(ivs.shape) != (n, 16) or ivs.device != device:
+            raise ValueError("per-message ivs must be an N x 16 CUDA tensor on the input's device")
+        return ivs, None
+    return None, _host_bytes(ivs, 16, "iv")
+
+
+def cbc_encrypt(x: torch.Tensor, round_keys, ivs=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """CBC over each row of an N x M grid; ivs: shared 16-byte IV or N x 16 CUDA tensor."""
+    x, out = _check_grid(x, out)
+    rk = _host_bytes(round_keys, 176, "round_keys")
+    d_ivs, ivb = _ivs(ivs, x.shape[0], x.device)
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.lib().gaes_cbc_encrypt_dev(_p(x), _p(out), x.shape[0], x.shape[1], _p(d_ivs), _p(ivb),
+                                                   _p(rk), _stream()))
+    return out
+
+
+def cbc_decrypt(x: torch.Tensor, round_keys, ivs=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    x, out = _check_grid(x, out)
+    rk = _host_bytes(round_keys, 176, "round_keys")
+    d_ivs, ivb = _ivs(ivs, x.shape[0], x.device)
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.lib().gaes_cbc_decrypt_dev(_p(x), _p(out), x.shape[0], x.shape[1], _p(d_ivs), _p(ivb),
+                                                   _p(rk), _stream()))
+    return out
+
+
+def expand_keys(keys: torch.Tensor, with_decrypt: bool = True):
+    """K x 16 CUDA keys -> (rk_enc K x 11 x 16, rk_dec K x 11 x 16 or None)."""
+    keys = _u8_cuda(keys, "keys", 2)
+    if keys.shape[1] != 16:
+        raise ValueError("keys must be K x 16")
+    k = keys.shape[0]
+    rk_enc = torch.empty((k, 11, 16), dtype=torch.uint8, device=keys.device)
+    rk_dec = torch.empty_like(rk_enc) if with_decrypt else None
+    with torch.cuda.device(keys.device):
+        _lib.check(_lib.lib().gaes_expand_keys_dev(_p(keys), k, _p(rk_enc), _p(rk_dec), _stream()))
+    return rk_enc, rk_dec
+
+
+def expand_key(key: bytes, device=None) -> np.ndarray:
+    """One key -> u8[11,16] round keys on the host (GPU key schedule)."""
+    kb = _host_bytes(key, 16, "key")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    rk, _ = expand_keys(torch.from_numpy(kb.copy()).view(1, 16).to(dev), with_decrypt=False)
+    return rk[0].cpu().numpy()
+
+
+def _many_key(enc: bool, x, rks, ivs, out):
+    x, out = _check_grid(x, out)
+    if x.shape[1] != 16:
+        raise ValueError("many-key batches are N x 16 rows")
+    rks = _u8_cuda(rks, "round_keys", 3)
+    k = rks.shape[0]
+    if tuple(rks.shape[1:]) != (11, 16) or k == 0 or x.shape[0] % k:
+        raise ValueError("round_keys must be K x 11 x 16 and N a multiple of K")
+    if ivs is not None:
+        ivs = _u8_cuda(ivs, "ivs", 2)
+        if tuple(ivs.shape) != (k, 16):
+            raise ValueError("ivs must be K x 16")
+    bpk = x.shape[0] // k
+    fn = _lib.lib().gaes_many_key_encrypt_dev if enc else _lib.lib().gaes_many_key_decrypt_dev
+    with torch.cuda.device(x.device):
+        _lib.check(fn(_p(x), _p(out), bpk, k, _p(rks), _p(ivs), _stream()))
+    return out
+
+
+def many_key_encrypt(x: torch.Tensor, rk_enc: torch.Tensor, ivs: torch.Tensor | None = None,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+    """Key i encrypts rows [i*N/K, (i+1)*N/K) with its own shared IV ivs[i]."""
+    return _many_key(True, x, rk_enc, ivs, out)
+
+
+def many_key_decrypt(x: torch.Tensor, rk_dec: torch.Tensor, ivs: torch.Tensor | None = None,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+    """Inverse of many_key_encrypt; rk_dec from expand_keys(..., with_decrypt=True)."""
+    return _many_key(False, x, rk_dec, ivs, out)
+
+
+def gf_tables(device: int = 0):
+    """Device GF layer output: (sbox, inv_sbox, te[4,256], td[4,256]) on the host."""
+    s = np.empty(256, np.uint8)
+    si = np.empty(256, np.uint8)
+    te = np.empty(1024, np.uint32)
+    td = np.empty(1024, np.uint32)
+    _lib.check(_lib.lib().gaes_gf_tables(int(device), _p(s), _p(si), _p(te), _p(td)))
+    return s, si, te.reshape(4, 256), td.reshape(4, 256)

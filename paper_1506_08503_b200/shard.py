@@ -1,0 +1,85 @@
+"""Multi-GPU shard plan (north_star subsystem (4)).
+
+The reference's data parallelism is a balanced contiguous row partition
+(parallel.py:37-50, ``plan``) fanned out over threads (:66-75).  On an
+8 x B200 box the same plan assigns contiguous block ranges to GPUs -- one
+process (rank) per GPU, one stream each, no collective on the data path
+because blocks are independent.  Only timing and the
+optional verification reduce across ranks.
+
+``plan`` is pure Python (CPU-testable); ``rank_slice`` / ``key_slice`` give a
+rank its share; ``max_over_ranks`` is the one reduction the bench performs.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class ParallelPlan:
+    """Balanced contiguous partition of [0, N) into at most `workers` chunks."""
+
+    workers: int
+    chunks: tuple
+
+    def __post_init__(self):
+        if self.workers < 1:
+            raise ValueError("need at least one worker")
+
+
+def plan(n_messages: int, workers: int) -> ParallelPlan:
+    """parallel.py:37-50: contiguous chunks whose sizes differ by at most 1."""
+    if workers < 1:
+        raise ValueError("need at least one worker")
+    if n_messages < 0:
+        raise ValueError("negative message count")
+    used = min(workers, n_messages)
+    chunks = []
+    start = 0
+    for i in range(used):
+        size = n_messages // used + (1 if i < n_messages % used else 0)
+        chunks.append((start, start + size))
+        start += size
+    return ParallelPlan(workers=workers, chunks=tuple(chunks))
+
+
+def rank_slice(n_messages: int, rank: int, world_size: int) -> tuple:
+    """Rows [lo, hi) owned by `rank` (empty range if the plan has fewer chunks)."""
+    if not 0 <= rank < world_size:
+        raise ValueError("rank out of range")
+    chunks = plan(n_messages, world_size).chunks
+    return chunks[rank] if rank < len(chunks) else (n_messages, n_messages)
+
+
+def key_slice(n_keys: int, rank: int, world_size: int) -> tuple:
+    """Config 5 shards keys (and with them their blocks) contiguously."""
+    return rank_slice(n_keys, rank, world_size)
+
+
+def dist_env() -> tuple:
+    """(rank, local_rank, world_size) from the torchrun environment (defaults 0, 0, 1)."""
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """All-reduce MAX of a per-rank scalar (timing); identity without a process group."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(value: int, device=None) -> int:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return int(value)
+    t = torch.tensor([int(value)], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return int(t.item())

@@ -1,0 +1,117 @@
+"""CPU-only checks of the C ABI library and the host-side logic (no GPU calls).
+
+* libgaes_b200.so loads and exports every function include/gaes_b200.h
+  declares, with the ctypes signature table matching the header;
+* the cubin inside it targets sm_100a;
+* backend_cuda validates arguments like the reference's compiled kernel
+  (Cython buffer errors, probe P11) before any device work;
+* without a GPU the product path fails loudly instead of falling back.
+"""
+
+import os
+import re
+import shutil
+import subprocess
+
+import numpy as np
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(REPO, "include", "gaes_b200.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"GAES_API\s+[\w\s\*]+?\b(gaes_\w+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1506_08503_b200 import _build
+    _build.build()
+    from paper_1506_08503_b200 import _lib
+    return _lib
+
+
+def test_header_declares_the_backend_contract():
+    names = _declared()
+    for required in ("gaes_cbc_encrypt", "gaes_cbc_decrypt", "gaes_expand_keys_dev", "gaes_gf_tables",
+                     "gaes_encrypt_blocks_dev", "gaes_many_key_encrypt_dev", "gaes_last_error"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.check_output(["nm", "-D", "--defined-only", lib.LIB_PATH], text=True)
+    exported = set(re.findall(r"\bT (gaes_\w+)", out))
+    missing = [n for n in _declared() if n not in exported]
+    assert not missing, missing
+    L = lib.lib()
+    for name in _declared():
+        assert hasattr(L, name)
+
+
+def test_signature_table_covers_header(lib):
+    assert sorted(lib.SIGNATURES) == _declared()
+    text = open(HEADER).read()
+    for name, (_, args) in lib.SIGNATURES.items():
+        m = re.search(r"\b%s\s*\(([^)]*)\)" % name, text)
+        params = [p for p in m.group(1).split(",") if p.strip() and p.strip() != "void"]
+        assert len(params) == len(args), name
+
+
+def test_cubin_is_sm_100a(lib):
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not on PATH")
+    out = subprocess.check_output(["cuobjdump", "--list-elf", lib.LIB_PATH], text=True)
+    assert "sm_100a" in out
+
+
+def test_version_and_device_count_without_gpu(lib):
+    L = lib.lib()
+    assert L.gaes_version() >= 10000
+    assert lib.device_count() >= 0
+
+
+def test_no_cpu_fallback_without_gpu(lib, oracle):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1506_08503_b200 import backend_cuda
+    t = oracle.encrypt_tables(bytes(16))
+    data = np.zeros((4, 16), np.uint8)
+    with pytest.raises(lib.GaesError, match="no CUDA device"):
+        backend_cuda.cbc_encrypt(data, np.zeros((4, 16), np.uint8), *t, np.empty_like(data))
+
+
+def test_backend_argument_errors(lib, oracle):
+    from paper_1506_08503_b200 import backend_cuda
+    t = oracle.encrypt_tables(bytes(16))
+    good = np.zeros((4, 16), np.uint8)
+    ivs = np.zeros((4, 16), np.uint8)
+    with pytest.raises(ValueError, match="dtype mismatch"):
+        backend_cuda.cbc_encrypt(good.astype(np.int8), ivs, *t, np.empty_like(good))
+    with pytest.raises(ValueError, match="C-contiguous"):
+        backend_cuda.cbc_encrypt(np.zeros((4, 32), np.uint8)[:, ::2], ivs, *t, np.empty_like(good))
+    ro = np.empty_like(good)
+    ro.setflags(write=False)
+    with pytest.raises(ValueError, match="read-only"):
+        backend_cuda.cbc_encrypt(good, ivs, *t, ro)
+    with pytest.raises(ValueError, match="wrong number of dimensions"):
+        backend_cuda.cbc_encrypt(good.reshape(-1), ivs, *t, np.empty_like(good))
+    with pytest.raises(ValueError, match="ivs"):
+        backend_cuda.cbc_encrypt(good, ivs[:3], *t, np.empty_like(good))
+    with pytest.raises(ValueError, match="multiple of 16"):
+        backend_cuda.cbc_encrypt(np.zeros((4, 20), np.uint8), ivs, *t, np.zeros((4, 20), np.uint8))
+    # N == 0 is a no-op, like the reference (probe P11)
+    backend_cuda.cbc_encrypt(np.empty((0, 16), np.uint8), np.empty((0, 16), np.uint8), *t,
+                             np.empty((0, 16), np.uint8))
+
+
+def test_product_package_does_not_import_the_oracle():
+    pkg = os.path.join(REPO, "paper_1506_08503_b200")
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cpp", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(root, f)).read()
+                assert "from oracle" not in text and "import oracle" not in text, f
+                assert "liboracle" not in text and "oracle/_ref" not in text, f

@@ -1,0 +1,373 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, bit-exact.
+
+Mirrors the reference's hot-path tests (pkg/tests/test_aes_cbc.py,
+test_backends.py, test_key_schedule.py, test_parallel.py) with the cuda
+backend / device API in place of the compiled kernel, plus the north-star
+configs at full size through size-independent properties.
+"""
+
+import hashlib
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1506_08503_b200 import _lib, backend_cuda, device  # noqa: E402
+
+NIST_KEY = bytes.fromhex("2b7e151628aed2a6abf7158809cf4f3c")
+NIST_IV = bytes.fromhex("000102030405060708090a0b0c0d0e0f")
+NIST_PT = bytes.fromhex(
+    "6bc1bee22e409f96e93d7e117393172aae2d8a571e03ac9c9eb76fac45af8e51"
+    "30c81c46a35ce411e5fbc1191a0a52eff69f2445df4f9b17ad2b417be66c3710")
+NIST_CT = bytes.fromhex(
+    "7649abac8119b246cee98e9b12e9197d5086cb9b507219ee95db113a917678b2"
+    "73bed6b8e3c1743b7116e69e222295163ff1caa1681fac09120eca307586e1a7")
+
+
+def _cuda_enc(key, ivrows, data, oracle):
+    out = np.empty_like(data)
+    backend_cuda.cbc_encrypt(data, ivrows, *oracle.encrypt_tables(key), out)
+    return out
+
+
+def _cuda_dec(key, ivrows, data, oracle):
+    out = np.empty_like(data)
+    backend_cuda.cbc_decrypt(data, ivrows, *oracle.decrypt_tables(key), out)
+    return out
+
+
+# ---------------------------------------------------------------- GF layer
+
+def test_gf_layer_tables_match_oracle(oracle, golden):
+    s, si, te, td = device.gf_tables(0)
+    assert np.array_equal(s, golden["sbox"])
+    assert np.array_equal(si, golden["inv_sbox"])
+    fwd = golden["mix_fwd"]
+    inv = golden["mix_inv"]
+    for j in range(4):
+        for x in (0, 1, 0x53, 0xFF):
+            want = sum(int(fwd[r, j, s[x]]) << (8 * r) for r in range(4))
+            assert te[j, x] == want
+            want = sum(int(inv[r, j, si[x]]) << (8 * r) for r in range(4))
+            assert td[j, x] == want
+    assert te[0, 0] == 0xA56363C6  # survey probe P10
+
+
+def test_tables_are_standard(oracle):
+    L = _lib.lib()
+    t = oracle.encrypt_tables(bytes(16))
+    p = lambda a: a.__array_interface__["data"][0]  # noqa: E731
+    assert L.gaes_tables_are_standard(p(t[1]), p(np.ascontiguousarray(t[2])), p(t[3]), 0) == 1
+    td = oracle.decrypt_tables(bytes(16))
+    assert L.gaes_tables_are_standard(p(td[1]), p(np.ascontiguousarray(td[2])), p(td[3]), 1) == 1
+    bad = t[1].copy()
+    bad[0] ^= 1
+    assert L.gaes_tables_are_standard(p(bad), p(np.ascontiguousarray(t[2])), p(t[3]), 0) == 0
+
+
+# ---------------------------------------------------------------- KATs
+
+def test_fips197_block_kat(oracle):
+    key = bytes.fromhex("000102030405060708090a0b0c0d0e0f")
+    pt = np.frombuffer(bytes.fromhex("00112233445566778899aabbccddeeff"), np.uint8).reshape(1, 16)
+    iv0 = np.zeros((1, 16), np.uint8)
+    ct = _cuda_enc(key, iv0, pt, oracle)
+    assert ct.tobytes() == bytes.fromhex("69c4e0d86a7b0430d8cdb78070b4c55a")
+    assert np.array_equal(_cuda_dec(key, iv0, ct, oracle), pt)
+
+
+def test_sp800_38a_cbc_four_blocks(oracle):
+    pt = np.frombuffer(NIST_PT, np.uint8).reshape(1, 64)
+    iv = np.frombuffer(NIST_IV, np.uint8).reshape(1, 16)
+    ct = _cuda_enc(NIST_KEY, iv, pt, oracle)
+    assert ct.tobytes() == NIST_CT
+    assert _cuda_dec(NIST_KEY, iv, ct, oracle).tobytes() == NIST_PT
+
+
+def test_golden_cases_from_reference(oracle, golden, golden_meta):
+    for case in golden_meta["cases"]:
+        i = case["idx"]
+        key = golden[f"case{i}_key"].tobytes()
+        iv = golden[f"case{i}_iv"]
+        ct = _cuda_enc(key, iv, golden[f"case{i}_pt"], oracle)
+        assert np.array_equal(ct, golden[f"case{i}_ct"]), case
+        assert np.array_equal(_cuda_dec(key, iv, ct, oracle), golden[f"case{i}_pt"]), case
+
+
+# ---------------------------------------------------------------- backend contract
+
+@pytest.mark.parametrize("n,blocks", [(1, 1), (3, 1), (1, 5), (17, 3), (64, 2), (5, 4), (32, 2), (1023, 1),
+                                      (4097, 1), (300, 9)])
+@pytest.mark.parametrize("shared", [True, False])
+def test_backend_matches_oracle(oracle, n, blocks, shared):
+    rng = np.random.default_rng(n * 100 + blocks + (7 if shared else 0))
+    key = rng.bytes(16)
+    data = rng.integers(0, 256, (n, 16 * blocks), dtype=np.uint8)
+    if shared:
+        ivs = np.tile(rng.integers(0, 256, 16, dtype=np.uint8), (n, 1))
+    else:
+        ivs = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    want = oracle.encrypt(key, ivs, data)
+    got = _cuda_enc(key, ivs, data, oracle)
+    assert np.array_equal(got, want)
+    assert np.array_equal(_cuda_dec(key, ivs, got, oracle), data)
+
+
+def test_empty_batch_is_noop(oracle):
+    data = np.empty((0, 16), np.uint8)
+    out = np.empty((0, 16), np.uint8)
+    backend_cuda.cbc_encrypt(data, np.empty((0, 16), np.uint8), *oracle.encrypt_tables(bytes(16)), out)
+
+
+def test_nonstandard_tables_use_generic_path(oracle):
+    """Any tables are honoured, like the reference kernel (tables in, no cipher knowledge)."""
+    rng = np.random.default_rng(11)
+    key = rng.bytes(16)
+    n = 257
+    data = rng.integers(0, 256, (n, 32), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    rk, box, lut, perm = oracle.encrypt_tables(key)
+    box2 = np.ascontiguousarray(box[rng.permutation(256)])       # another bijection
+    perm2 = np.ascontiguousarray(rng.permutation(16).astype(np.uint8))  # another gather
+    lut2 = np.ascontiguousarray(rng.integers(0, 256, (4, 4, 256), dtype=np.uint8))  # non-linear
+    for tb in [(rk, box2, lut, perm), (rk, box, lut2, perm), (rk, box, lut, perm2), (rk, box2, lut2, perm2)]:
+        want = np.empty_like(data)
+        oracle.cbc_encrypt(data, ivs, *tb, want)
+        got = np.empty_like(data)
+        backend_cuda.cbc_encrypt(data, ivs, *tb, got)
+        assert np.array_equal(got, want)
+        wantd = np.empty_like(data)
+        oracle.cbc_decrypt(data, ivs, *tb, wantd)
+        gotd = np.empty_like(data)
+        backend_cuda.cbc_decrypt(data, ivs, *tb, gotd)
+        assert np.array_equal(gotd, wantd)
+
+
+def test_concurrent_calls_on_disjoint_slices(oracle):
+    """parallel._run_chunks calls the backend from worker threads (parallel.py:66-75)."""
+    rng = np.random.default_rng(3)
+    key = rng.bytes(16)
+    n = 20000
+    data = rng.integers(0, 256, (n, 32), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    tables = oracle.encrypt_tables(key)
+    out = np.empty_like(data)
+    chunks = oracle.plan(n, 7)
+    errs = []
+
+    def work(lo, hi):
+        try:
+            backend_cuda.cbc_encrypt(data[lo:hi], ivs[lo:hi], *tables, out[lo:hi])
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=c) for c in chunks]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    assert not errs
+    assert np.array_equal(out, oracle.encrypt(key, ivs, data, threads=4))
+
+
+def test_pinned_host_buffers(oracle):
+    rng = np.random.default_rng(12)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    n = 1 << 18
+    pin_in = torch.empty((n, 16), dtype=torch.uint8).pin_memory()
+    pin_out = torch.empty((n, 16), dtype=torch.uint8).pin_memory()
+    p = pin_in.numpy()
+    p[:] = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    rk = oracle.gen_keys(key)
+    backend_cuda.encrypt_shared_iv(p, iv, rk, out=pin_out.numpy())
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (n, 1))
+    assert np.array_equal(pin_out.numpy(), oracle.encrypt(key, ivrows, p, threads=4))
+    back = backend_cuda.decrypt_shared_iv(pin_out.numpy(), iv, rk)
+    assert np.array_equal(back, p)
+
+
+def test_shared_iv_entry_wide_rows(oracle):
+    rng = np.random.default_rng(13)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    data = rng.integers(0, 256, (999, 48), dtype=np.uint8)
+    rk = oracle.gen_keys(key)
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (999, 1))
+    ct = backend_cuda.encrypt_shared_iv(data, iv, rk)
+    assert np.array_equal(ct, oracle.encrypt(key, ivrows, data))
+    assert np.array_equal(backend_cuda.decrypt_shared_iv(ct, iv, rk), data)
+
+
+def test_argument_errors_match_reference(oracle):
+    t = oracle.encrypt_tables(bytes(16))
+    good = np.zeros((4, 16), np.uint8)
+    ivs = np.zeros((4, 16), np.uint8)
+    with pytest.raises(ValueError, match="dtype mismatch"):
+        backend_cuda.cbc_encrypt(good.astype(np.float64), ivs, *t, np.empty_like(good))
+    with pytest.raises(ValueError, match="C-contiguous"):
+        backend_cuda.cbc_encrypt(np.zeros((4, 32), np.uint8)[:, ::2], ivs, *t, np.empty_like(good))
+    ro = np.empty_like(good)
+    ro.setflags(write=False)
+    with pytest.raises(ValueError, match="read-only"):
+        backend_cuda.cbc_encrypt(good, ivs, *t, ro)
+    with pytest.raises(ValueError, match="dimensions"):
+        backend_cuda.cbc_encrypt(good.reshape(-1), ivs, *t, np.empty_like(good))
+    with pytest.raises(ValueError, match="multiple of 16"):
+        backend_cuda.cbc_encrypt(np.zeros((4, 20), np.uint8), ivs, *t, np.zeros((4, 20), np.uint8))
+
+
+# ---------------------------------------------------------------- device API
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 1000, 148 * 1024 * 2 + 17])
+def test_device_blocks_ragged_sizes(oracle, n):
+    rng = np.random.default_rng(n)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    p = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    rk = oracle.gen_keys(key)
+    x = torch.from_numpy(p).cuda()
+    c = device.encrypt_blocks(x, rk, iv)
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (n, 1))
+    assert np.array_equal(c.cpu().numpy(), oracle.encrypt(key, ivrows, p, threads=4))
+    assert np.array_equal(device.decrypt_blocks(c, rk, iv).cpu().numpy(), p)
+
+
+@pytest.mark.parametrize("blocks", [1, 2, 7])
+def test_device_cbc_grids(oracle, blocks):
+    rng = np.random.default_rng(50 + blocks)
+    key = rng.bytes(16)
+    n = 3001
+    p = rng.integers(0, 256, (n, 16 * blocks), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    rk = oracle.gen_keys(key)
+    x = torch.from_numpy(p).cuda()
+    d_ivs = torch.from_numpy(ivs).cuda()
+    c = device.cbc_encrypt(x, rk, d_ivs)
+    assert np.array_equal(c.cpu().numpy(), oracle.encrypt(key, ivs, p))
+    assert np.array_equal(device.cbc_decrypt(c, rk, d_ivs).cpu().numpy(), p)
+    iv = rng.bytes(16)
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (n, 1))
+    c2 = device.cbc_encrypt(x, rk, iv)
+    assert np.array_equal(c2.cpu().numpy(), oracle.encrypt(key, ivrows, p))
+    assert np.array_equal(device.cbc_decrypt(c2, rk, iv).cpu().numpy(), p)
+
+
+# ---------------------------------------------------------------- key schedule
+
+def test_gpu_key_schedule_matches_reference(oracle, golden):
+    keys = torch.from_numpy(golden["keys"]).cuda()
+    rk_enc, rk_dec = device.expand_keys(keys)
+    assert np.array_equal(rk_enc.cpu().numpy(), golden["round_keys"])
+    # decrypt form: rows 1..9 are InvMixColumns of the forward rows
+    inv = golden["mix_inv"]
+    d = rk_dec.cpu().numpy()
+    e = golden["round_keys"]
+    assert np.array_equal(d[:, 0], e[:, 0]) and np.array_equal(d[:, 10], e[:, 10])
+    for k in (0, 5, 200):
+        for r in range(1, 10):
+            for c in range(4):
+                col = e[k, r, 4 * c:4 * c + 4]
+                want = [inv[row, 0, col[0]] ^ inv[row, 1, col[1]] ^ inv[row, 2, col[2]] ^ inv[row, 3, col[3]]
+                        for row in range(4)]
+                assert list(d[k, r, 4 * c:4 * c + 4]) == want
+
+
+def test_gpu_key_schedule_1000_random_keys(oracle):
+    rng = np.random.default_rng(1000)
+    keys = rng.integers(0, 256, (1000, 16), dtype=np.uint8)
+    rk_enc, _ = device.expand_keys(torch.from_numpy(keys).cuda(), with_decrypt=False)
+    assert np.array_equal(rk_enc.cpu().numpy(), oracle.gen_keys_batch(keys))
+
+
+# ---------------------------------------------------------------- north-star configs
+
+def _cfg_inputs(n, seed=2016):
+    rng = np.random.default_rng(seed)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    return rng, key, iv
+
+
+def test_config1_full_digest(oracle, golden_meta):
+    d = golden_meta["digests"]["65536"]
+    rng, key, iv = _cfg_inputs(1 << 16)
+    p = rng.integers(0, 256, (1 << 16, 16), dtype=np.uint8)
+    rk = oracle.gen_keys(key)
+    # drop-in path: host buffers, tiled IV rows
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (p.shape[0], 1))
+    c = _cuda_enc(key, ivrows, p, oracle)
+    assert hashlib.sha256(c.tobytes()).hexdigest() == d["sha256_c"]
+    assert np.array_equal(_cuda_dec(key, ivrows, c, oracle), p)
+    # device path
+    cd = device.encrypt_blocks(torch.from_numpy(p).cuda(), rk, iv).cpu().numpy()
+    assert hashlib.sha256(cd.tobytes()).hexdigest() == d["sha256_c"]
+
+
+def test_config2_digest_subset_and_round_trip(oracle, golden_meta):
+    n = 1 << 24
+    d = golden_meta["digests"][str(n)]
+    rng, key, iv = _cfg_inputs(n)
+    p = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    rk = oracle.gen_keys(key)
+    x = torch.from_numpy(p).cuda()
+    c = device.encrypt_blocks(x, rk, iv)
+    ch = c.cpu().numpy()
+    assert hashlib.sha256(ch.tobytes()).hexdigest() == d["sha256_c"]
+    # seeded 1% subset vs the oracle (rows are independent)
+    rng2 = np.random.default_rng(7)
+    idx = np.sort(rng2.choice(n, n // 100, replace=False))
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (idx.size, 1))
+    assert np.array_equal(ch[idx], oracle.encrypt(key, ivrows, p[idx], threads=8))
+    back = device.decrypt_blocks(c, rk, iv)
+    assert torch.equal(back, x)
+
+
+def test_config4_determinism_equal_plaintexts(oracle):
+    """Deterministic (shared-IV) encryption: equal P -> equal C, #unique preserved."""
+    rng = np.random.default_rng(4)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    vals = rng.integers(0, 2**63, 5000, dtype=np.int64).astype(np.uint64)
+    ranks = rng.zipf(1.5, 200000) % vals.size
+    p = np.zeros((ranks.size, 16), np.uint8)
+    p[:, :8] = vals[ranks].view(np.uint8).reshape(-1, 8)
+    rk = oracle.gen_keys(key)
+    c = device.encrypt_blocks(torch.from_numpy(p).cuda(), rk, iv).cpu().numpy()
+    up, inv_p = np.unique(p, axis=0, return_inverse=True)
+    uc, inv_c = np.unique(c, axis=0, return_inverse=True)
+    assert up.shape[0] == uc.shape[0]
+    # the map P -> C is a function: each P class lands on one C class
+    first = {}
+    for a, b in zip(inv_p.ravel()[:20000], inv_c.ravel()[:20000]):
+        assert first.setdefault(int(a), int(b)) == int(b)
+    idx = np.arange(0, ranks.size, 97)
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (idx.size, 1))
+    assert np.array_equal(c[idx], oracle.encrypt(key, ivrows, p[idx]))
+
+
+def test_config5_many_key(oracle):
+    rng = np.random.default_rng(5)
+    k, bpk = 64, 4099
+    keys = rng.integers(0, 256, (k, 16), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (k, 16), dtype=np.uint8)
+    p = rng.integers(0, 256, (k * bpk, 16), dtype=np.uint8)
+    d_keys = torch.from_numpy(keys).cuda()
+    rk_enc, rk_dec = device.expand_keys(d_keys)
+    assert np.array_equal(rk_enc.cpu().numpy(), oracle.gen_keys_batch(keys))
+    x = torch.from_numpy(p).cuda()
+    d_ivs = torch.from_numpy(ivs).cuda()
+    c = device.many_key_encrypt(x, rk_enc, d_ivs)
+    ch = c.cpu().numpy()
+    for i in (0, 1, 31, 63):
+        rows = slice(i * bpk, (i + 1) * bpk)
+        ivrows = np.tile(ivs[i], (bpk, 1))
+        assert np.array_equal(ch[rows], oracle.encrypt(keys[i].tobytes(), ivrows, p[rows])), i
+    assert torch.equal(device.many_key_decrypt(c, rk_dec, d_ivs), x)
+
+
+def test_launch_counter_and_kernel_name(oracle):
+    before = _lib.launch_count()
+    x = torch.zeros((1024, 16), dtype=torch.uint8, device="cuda")
+    device.encrypt_blocks(x, oracle.gen_keys(bytes(16)))
+    assert _lib.launch_count() == before + 1
+    assert _lib.last_kernel().startswith("k_blocks_enc")
