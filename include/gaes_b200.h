@@ -156,6 +156,11 @@ GAES_API int gaes_many_key_decrypt_dev(const void *in, void *out, size_t blocks_
 GAES_API uint64_t gaes_launch_count(void);
 /* Name of the kernel variant the last M=16 encrypt used ("ttable_ilp2", ...). */
 GAES_API const char *gaes_last_kernel(void);
+/* Roofline probe: run the encrypt round function on register-resident
+ * states (no HBM traffic), `iters` encryptions per thread on every SM, and
+ * report the achieved table-lookup rate (160 lookups per encryption) -- the
+ * measured ceiling of the shared-memory T-table formulation. */
+GAES_API int gaes_probe_round_rate(int device, uint32_t iters, double *lookups_per_sec, double *ms);
 /* Select the M=16 encrypt/decrypt formulation: 0 = auto (fastest measured),
  * 1 = T-table in shared memory, 2 = bitsliced.  Returns the value set or
  * GAES_EINVAL if the variant is not built. */

@@ -628,6 +628,38 @@ GAES_API int gaes_set_variant(int variant) {
   return variant;
 }
 
+GAES_API int gaes_probe_round_rate(int device, uint32_t iters, double* lookups_per_sec, double* ms) {
+  DevCtx* c = nullptr;
+  int rc = get_ctx(device, &c);
+  if (rc) return rc;
+  int prev = 0;
+  GAES_CK(cudaGetDevice(&prev));
+  GAES_CK(cudaSetDevice(device));
+  uint32_t* sink = nullptr;
+  GAES_CK(cudaMalloc(&sink, 4));
+  uint8_t rk[176] = {0};
+  const RoundKeys k = make_enc_keys(rk, nullptr, false);
+  cudaEvent_t a, b;
+  GAES_CK(cudaEventCreate(&a));
+  GAES_CK(cudaEventCreate(&b));
+  GAES_CK(launch_round_probe(c->d_std_enc, k, 16, sink, c->sms, 0));  // warm-up
+  GAES_CK(cudaEventRecord(a, 0));
+  GAES_CK(launch_round_probe(c->d_std_enc, k, iters, sink, c->sms, 0));
+  GAES_CK(cudaEventRecord(b, 0));
+  GAES_CK(cudaEventSynchronize(b));
+  note_kernel("k_round_probe");
+  float t = 0;
+  GAES_CK(cudaEventElapsedTime(&t, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  cudaSetDevice(prev);
+  const double lookups = (double)c->sms * kBlockThreads * (double)iters * 160.0;
+  if (lookups_per_sec) *lookups_per_sec = lookups / (t / 1e3);
+  if (ms) *ms = t;
+  return GAES_OK;
+}
+
 GAES_API int gaes_gf_tables(int device, uint8_t sbox[256], uint8_t inv_sbox[256], uint32_t te[1024],
                             uint32_t td[1024]) {
   DevCtx* c = nullptr;

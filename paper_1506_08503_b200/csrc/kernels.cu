@@ -321,6 +321,22 @@ __global__ void __launch_bounds__(kManyKeyThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Roofline probe: the encrypt round function on register-resident states,
+// no HBM traffic, `iters` full encryptions per thread.  Its lookup rate is
+// the measured ceiling of the shared-memory T-table formulation on this GPU
+// (reported beside the nominal 32 lanes/clk/SM figure).
+__global__ void __launch_bounds__(kBlockThreads, 1)
+    k_round_probe(const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk, uint32_t iters,
+                  uint32_t* __restrict__ sink) {
+  extern __shared__ __align__(1024) char smem[];
+  fill_tables(smem, compact);
+  const uint32_t lb = (threadIdx.x & 31) * 4;
+  uint32_t s0 = threadIdx.x, s1 = blockIdx.x, s2 = threadIdx.x * 7, s3 = ~threadIdx.x;
+  for (uint32_t i = 0; i < iters; i++) encrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
+  if ((s0 ^ s1 ^ s2 ^ s3) == 0x12345678u) sink[0] = s0;  // keep the work alive
+}
+
+// ---------------------------------------------------------------------------
 // Launchers.
 
 static int grid_for(uint64_t work_items, int per_thread, int sms, int cta_threads = kBlockThreads) {
@@ -392,6 +408,14 @@ cudaError_t launch_generic(bool dec, const uint8_t* data, const uint8_t* ivs, ui
     k_generic_cbc<true><<<(int)ctas, 128, 0, s>>>(data, ivs, n, m, rk, box, lut, perm, out);
   else
     k_generic_cbc<false><<<(int)ctas, 128, 0, s>>>(data, ivs, n, m, rk, box, lut, perm, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_round_probe(const uint32_t* compact, const RoundKeys& rk, uint32_t iters, uint32_t* sink,
+                               int sms, cudaStream_t s) {
+  cudaError_t e = set_smem(k_round_probe);
+  if (e != cudaSuccess) return e;
+  k_round_probe<<<sms, kBlockThreads, kSmemBytes, s>>>(compact, rk, iters, sink);
   return cudaGetLastError();
 }
 

@@ -23,6 +23,8 @@ cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint
 cudaError_t launch_generic(bool dec, const uint8_t* data, const uint8_t* ivs, uint64_t n, uint64_t m,
                            const uint8_t* rk, const uint8_t* box, const uint8_t* lut, const uint8_t* perm,
                            uint8_t* out, int sms, cudaStream_t s);
+cudaError_t launch_round_probe(const uint32_t* compact, const RoundKeys& rk, uint32_t iters, uint32_t* sink,
+                               int sms, cudaStream_t s);
 cudaError_t launch_expand_keys(const uint8_t* keys, uint64_t k, const uint32_t* compact_enc, uint8_t* rk_enc,
                                uint8_t* rk_dec, cudaStream_t s);
 cudaError_t launch_many_key(bool dec, const void* in, void* out, uint64_t bpk, uint64_t n_keys,
