@@ -285,7 +285,7 @@ def run_reference_impl(args):
     probe_n = 1 << 16
     t, kind = cpu_reference_rate(key, iv, probe_n, threads)
     rate = probe_n / max(t[0], 1e-9)
-    budget_per_step = 120.0 / max(1, args.steps + args.warmup)
+    budget_per_step = min(10.0, 120.0 / max(1, args.steps + args.warmup))
     n = int(min(w["blocks"] if args.config != 5 else 1 << 20, max(probe_n, rate * budget_per_step)))
     times, kind = cpu_reference_rate(key, iv, n, threads, reps=args.steps, warm=args.warmup)
     total = sum(times)

@@ -1,0 +1,127 @@
+"""Drop-in: the UNCHANGED reference package running on the cuda backend.
+
+The reference (pip-installed into baseline/_ref by scripts/stage_reference.sh)
+keeps its entry points -- encrypt_batch / decrypt_batch (aes_cbc.py:345-368),
+encrypt_batch_parallel / decrypt_batch_parallel (parallel.py:78-105) -- and
+only its backend registry (backend.py:17-64) gains NAME="cuda".  Results
+must be byte-identical to the reference's own compiled backend.  When the
+reference's test files are staged (baseline/_ref_tests) they are run
+unchanged with the cuda backend selected.
+"""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import REPO, reference_package_dir
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+REF = reference_package_dir()
+if REF is None:  # pragma: no cover
+    pytest.skip("reference package not staged (scripts/stage_reference.sh)", allow_module_level=True)
+
+
+@pytest.fixture(scope="module")
+def gaes():
+    sys.path.insert(0, REF)
+    import gaes as g
+    from paper_1506_08503_b200 import plugin
+    plugin.register(gaes_module=g)
+    yield g
+    g.backend.select("auto")
+
+
+def _both(gaes, fn):
+    """Run fn() under the compiled backend and under cuda; return both results."""
+    prev = gaes.backend.name()
+    try:
+        gaes.backend.select("compiled" if "compiled" in gaes.backend.available() else "numpy")
+        a = fn()
+        gaes.backend.select("cuda")
+        assert gaes.backend_name() == "cuda"
+        b = fn()
+    finally:
+        gaes.backend.select(prev)
+    return a, b
+
+
+def test_registry_round_trip(gaes):
+    assert "cuda" in gaes.backend.available()
+    gaes.backend.select("cuda")
+    assert gaes.backend.name() == "cuda"
+    gaes.backend.select(gaes.backend.name())  # test_backends.py:54-62 idiom
+    gaes.backend.select("auto")
+
+
+@pytest.mark.parametrize("n,width,shared", [(1, 16, True), (1000, 16, True), (1000, 16, False), (77, 48, True),
+                                            (77, 48, False), (3, 160, False)])
+def test_encrypt_decrypt_batch_identical(gaes, n, width, shared):
+    rng = np.random.default_rng(n * width + shared)
+    key = rng.bytes(16)
+    data = rng.integers(0, 256, (n, width), dtype=np.uint8)
+    batch = gaes.MessageBatch(data=data, original_lens=(width,) * n)
+    ivs = gaes.IVSet.shared(rng.bytes(16)) if shared else gaes.IVSet.per_message(
+        rng.integers(0, 256, (n, 16), dtype=np.uint8))
+    ct_ref, ct_gpu = _both(gaes, lambda: gaes.encrypt_batch(key, ivs, batch))
+    assert np.array_equal(ct_ref, ct_gpu)
+    pt_ref, pt_gpu = _both(gaes, lambda: gaes.decrypt_batch(key, ivs, ct_ref))
+    assert np.array_equal(pt_gpu, data) and np.array_equal(pt_ref, data)
+
+
+@pytest.mark.parametrize("workers", [1, 2, 3, 4, 7, 8])
+def test_parallel_entry_points_worker_independent(gaes, workers):
+    rng = np.random.default_rng(workers)
+    key = rng.bytes(16)
+    n = 5000
+    data = rng.integers(0, 256, (n, 32), dtype=np.uint8)
+    batch = gaes.MessageBatch(data=data, original_lens=(32,) * n)
+    ivs = gaes.IVSet.shared(rng.bytes(16))
+    ref, gpu = _both(gaes, lambda: gaes.encrypt_batch_parallel(key, ivs, batch, workers=workers))
+    assert np.array_equal(ref, gpu)
+    back = _both(gaes, lambda: gaes.decrypt_batch_parallel(key, ivs, gpu, workers=workers))[1]
+    assert np.array_equal(back, data)
+
+
+def test_config1_through_reference_entry_point(gaes, golden_meta):
+    import hashlib
+    d = golden_meta["digests"]["65536"]
+    rng = np.random.default_rng(2016)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    p = rng.integers(0, 256, (1 << 16, 16), dtype=np.uint8)
+    tables = gaes.aes_cbc._encrypt_tables(key)
+    ivrows = gaes.IVSet.shared(iv).rows(p.shape[0])
+    out = np.empty_like(p)
+    gaes.backend.select("cuda")
+    try:
+        gaes.backend.cbc_encrypt(p, ivrows, *tables, out)  # bench.py:127-136 boundary
+    finally:
+        gaes.backend.select("auto")
+    assert hashlib.sha256(out.tobytes()).hexdigest() == d["sha256_c"]
+
+
+def test_reference_test_suite_passes_on_cuda_backend():
+    """The reference's own hot-path tests, unchanged, with NAME="cuda" selected."""
+    tests_dir = os.path.join(REPO, "baseline", "_ref_tests")
+    if not os.path.isdir(tests_dir):
+        pytest.skip("reference tests not staged")
+    files = [os.path.join(tests_dir, f) for f in
+             ("test_aes_cbc.py", "test_parallel.py", "test_backends.py", "test_key_schedule.py",
+              "test_sbox_gen.py", "test_gf256.py")]
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([REF, REPO, env.get("PYTHONPATH", "")])
+    env.pop("GAES_BACKEND", None)
+    env["PYTHONDONTWRITEBYTECODE"] = "1"
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "paper_1506_08503_b200.plugin",
+                        "-p", "no:cacheprovider", "--rootdir", tests_dir, *files],
+                       cwd=tests_dir, env=env, capture_output=True, text=True, timeout=900)
+    tail = (r.stdout + r.stderr)[-3000:]
+    assert r.returncode == 0, tail
+    assert " passed" in tail and "failed" not in tail, tail
