@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/gaes_b200.h"
+#include "aes_bitslice.cuh"
 #include "gf.cuh"
 #include "kernels.h"
 
@@ -268,9 +269,26 @@ int tables_for(DevCtx* c, const uint8_t* box, const uint8_t* lut, uint32_t** out
   return GAES_OK;
 }
 
+// M = 16 shared-IV encrypt: the formulation chosen by measurement
+// (profiles/): T-table unless gaes_set_variant(2) selects the bitsliced kernel.
+cudaError_t launch_enc_folded(DevCtx* c, const void* in, void* out, uint64_t n, const uint32_t* compact,
+                              const RoundKeys& k, int ilp, cudaStream_t s);
+
 int ilp_default() {
   static int ilp = std::max(1, std::min(2, env_int("GAES_ILP", 2)));
   return ilp;
+}
+
+cudaError_t launch_enc_folded(DevCtx* c, const void* in, void* out, uint64_t n, const uint32_t* compact,
+                              const RoundKeys& k, int ilp, cudaStream_t s) {
+  if (g_variant.load() == 2) {
+    static thread_local BitsliceKeys bk;
+    bs_make_keys(k.w, bk);
+    note_kernel("k_bs_blocks");
+    return launch_bs_blocks(in, out, n, bk, c->sms, s);
+  }
+  note_kernel("k_blocks_enc_folded");
+  return launch_blocks(false, kIvFolded, ilp, in, out, n, compact, k, nullptr, 1, c->sms, s);
 }
 
 // --------------------------------------------------------------------------
@@ -345,9 +363,17 @@ int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t rows, const uint32_t* 
   const uint64_t nblk = rows * bpr;
   switch (j.mode) {
     case Mode::kFolded:
-      GAES_CK(launch_blocks(j.dec, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,
-                            c->sms, s.stream));
-      note_kernel(j.dec ? "k_blocks_dec_folded" : "k_blocks_enc_folded");
+      if (j.dec) {
+        GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,
+                              c->sms, s.stream));
+        note_kernel("k_blocks_dec_folded");
+      } else if (j.standard || g_variant.load() != 2) {
+        GAES_CK(launch_enc_folded(c, s.d_in, s.d_out, nblk, compact, j.rk, ilp_default(), s.stream));
+      } else {  // bitsliced kernel has the standard S-box built in; caller tables -> T-table
+        GAES_CK(launch_blocks(false, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,
+                              c->sms, s.stream));
+        note_kernel("k_blocks_enc_folded");
+      }
       break;
     case Mode::kChain:
       GAES_CK(launch_blocks(j.dec, kIvChain, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk,
@@ -623,7 +649,8 @@ GAES_API const char* gaes_last_kernel(void) {
 }
 
 GAES_API int gaes_set_variant(int variant) {
-  if (variant != 0 && variant != 1) return fail(GAES_EINVAL, "variant not built (0 = auto, 1 = T-table)");
+  if (variant < 0 || variant > 2)
+    return fail(GAES_EINVAL, "unknown variant (0 = auto, 1 = T-table, 2 = bitsliced)");
   g_variant.store(variant);
   return variant;
 }
@@ -718,9 +745,7 @@ GAES_API int gaes_encrypt_blocks_dev(const void* in, void* out, size_t n_blocks,
   int rc = current_ctx(&c);
   if (rc) return rc;
   const RoundKeys k = make_enc_keys(round_keys, iv, true);
-  GAES_CK(launch_blocks(false, kIvFolded, ilp_default(), in, out, n_blocks, c->d_std_enc, k, nullptr, 1, c->sms,
-                        (cudaStream_t)stream));
-  note_kernel("k_blocks_enc_folded");
+  GAES_CK(launch_enc_folded(c, in, out, n_blocks, c->d_std_enc, k, ilp_default(), (cudaStream_t)stream));
   return GAES_OK;
 }
 

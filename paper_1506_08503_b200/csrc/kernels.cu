@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "aes_bitslice.cuh"
 #include "aes_ttable.cuh"
 #include "gf.cuh"
 #include "kernels.h"
@@ -321,6 +322,36 @@ __global__ void __launch_bounds__(kManyKeyThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Bitsliced encrypt (M = 16, shared IV folded into the key masks): each warp
+// takes chunks of 1024 consecutive blocks; lane l holds blocks l, l+32, ...
+// (coalesced 512-byte loads), transposes them into 128 bit planes and runs
+// the LOP3 round function (aes_bitslice.cuh).  No shared memory.
+__global__ void __launch_bounds__(kBsThreads)
+    k_bs_blocks(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks,
+                const __grid_constant__ BitsliceKeys keys) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t n_chunks = (n_blocks + 1023) / 1024;
+  for (uint64_t ch = warp; ch < n_chunks; ch += n_warps) {
+    const uint64_t base = ch * 1024 + lane;
+    uint32_t st[128];
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+      const uint64_t b = base + 32 * k;
+      const uint4 v = b < n_blocks ? ld_stream(in + b) : make_uint4(0, 0, 0, 0);
+      st[4 * k + 0] = v.x; st[4 * k + 1] = v.y; st[4 * k + 2] = v.z; st[4 * k + 3] = v.w;
+    }
+    bs_encrypt32(st, keys);
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+      const uint64_t b = base + 32 * k;
+      if (b < n_blocks) st_stream(out + b, make_uint4(st[4 * k + 0], st[4 * k + 1], st[4 * k + 2], st[4 * k + 3]));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Roofline probe: the encrypt round function on register-resident states,
 // no HBM traffic, `iters` full encryptions per thread.  Its lookup rate is
 // the measured ceiling of the shared-memory T-table formulation on this GPU
@@ -378,6 +409,9 @@ cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* o
                           const uint32_t* compact, const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms,
                           cudaStream_t s) {
   if (n_blocks == 0) return cudaSuccess;
+  // Small batches: spread over every SM (one block per thread) rather than
+  // giving few CTAs two blocks per thread; the 192 KiB table fill is per CTA.
+  if ((uint64_t)sms * kBlockThreads * 8 > n_blocks) ilp = 1;
 #define GAES_CASE(I, D, M) \
   if (ilp == I && dec == D && ivmode == M) return launch_blocks_t<I, D, M>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s);
   GAES_CASE(1, false, kIvFolded) GAES_CASE(1, true, kIvFolded) GAES_CASE(1, false, kIvChain)
@@ -408,6 +442,18 @@ cudaError_t launch_generic(bool dec, const uint8_t* data, const uint8_t* ivs, ui
     k_generic_cbc<true><<<(int)ctas, 128, 0, s>>>(data, ivs, n, m, rk, box, lut, perm, out);
   else
     k_generic_cbc<false><<<(int)ctas, 128, 0, s>>>(data, ivs, n, m, rk, box, lut, perm, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bs_blocks(const void* in, void* out, uint64_t n_blocks, const BitsliceKeys& keys, int sms,
+                             cudaStream_t s) {
+  if (n_blocks == 0) return cudaSuccess;
+  const uint64_t chunks = (n_blocks + 1023) / 1024;
+  const uint64_t warps_per_cta = kBsThreads / 32;
+  uint64_t ctas = (chunks + warps_per_cta - 1) / warps_per_cta;
+  const uint64_t cap = (uint64_t)sms * kBsCtasPerSm;
+  if (ctas > cap) ctas = cap;
+  k_bs_blocks<<<(unsigned)ctas, kBsThreads, 0, s>>>((const uint4*)in, (uint4*)out, n_blocks, keys);
   return cudaGetLastError();
 }
 

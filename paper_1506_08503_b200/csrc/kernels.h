@@ -9,7 +9,9 @@
 namespace gaes {
 
 static constexpr int kBlockThreads = 1024;     // k_blocks / k_cbc_enc_rows: 1 CTA per SM
-static constexpr int kManyKeyThreads = 512;    // k_many_key: 44 round-key registers per thread
+static constexpr int kManyKeyThreads = 768;    // k_many_key: 44 round-key registers per thread (<= 85 regs)
+static constexpr int kBsThreads = 128;         // k_bs_blocks: ~170 registers per thread
+static constexpr int kBsCtasPerSm = 3;
 static constexpr int kIvFolded = 0;
 static constexpr int kIvChain = 1;
 
@@ -23,6 +25,9 @@ cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint
 cudaError_t launch_generic(bool dec, const uint8_t* data, const uint8_t* ivs, uint64_t n, uint64_t m,
                            const uint8_t* rk, const uint8_t* box, const uint8_t* lut, const uint8_t* perm,
                            uint8_t* out, int sms, cudaStream_t s);
+struct BitsliceKeys;
+cudaError_t launch_bs_blocks(const void* in, void* out, uint64_t n_blocks, const BitsliceKeys& keys, int sms,
+                             cudaStream_t s);
 cudaError_t launch_round_probe(const uint32_t* compact, const RoundKeys& rk, uint32_t iters, uint32_t* sink,
                                int sms, cudaStream_t s);
 cudaError_t launch_expand_keys(const uint8_t* keys, uint64_t k, const uint32_t* compact_enc, uint8_t* rk_enc,
