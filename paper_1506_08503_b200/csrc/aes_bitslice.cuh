@@ -181,7 +181,9 @@ BS_HD void bs_encrypt32(uint32_t* st, const BitsliceKeys& keys) {
   for (int c = 0; c < 4; c++) transpose32(a + 32 * c);
 #pragma unroll
   for (int i = 0; i < 128; i++) a[i] ^= keys.kp[0][i];
-#pragma unroll
+  // Rounds 1..9 stay a loop: one unrolled round body is ~2K instructions,
+  // ten of them overflow the instruction cache (ncu: stalled_no_instructions).
+#pragma unroll 1
   for (int r = 1; r < 10; r++) {
     bs_sub_bytes(a);
     uint32_t b[128];

@@ -367,7 +367,7 @@ int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t rows, const uint32_t* 
         GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,
                               c->sms, s.stream));
         note_kernel("k_blocks_dec_folded");
-      } else if (j.standard || g_variant.load() != 2) {
+      } else if (j.standard || g_variant.load() < 2) {
         GAES_CK(launch_enc_folded(c, s.d_in, s.d_out, nblk, compact, j.rk, ilp_default(), s.stream));
       } else {  // bitsliced kernel has the standard S-box built in; caller tables -> T-table
         GAES_CK(launch_blocks(false, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,

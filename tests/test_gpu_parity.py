@@ -373,8 +373,9 @@ def test_launch_counter_and_kernel_name(oracle):
     assert _lib.last_kernel().startswith("k_blocks_enc")
 
 
+@pytest.mark.parametrize("variant", [2])
 @pytest.mark.parametrize("n", [1, 1023, 1024, 1025, 148 * 384 * 32 + 999])
-def test_bitsliced_variant_matches_oracle(oracle, n):
+def test_bitsliced_variant_matches_oracle(oracle, n, variant):
     """The bitsliced LOP3 formulation (gaes_set_variant(2)) is bit-exact too."""
     L = _lib.lib()
     rng = np.random.default_rng(n + 99)
@@ -382,10 +383,10 @@ def test_bitsliced_variant_matches_oracle(oracle, n):
     p = rng.integers(0, 256, (n, 16), dtype=np.uint8)
     rk = oracle.gen_keys(key)
     try:
-        assert L.gaes_set_variant(2) == 2
+        assert L.gaes_set_variant(variant) == variant
         c = device.encrypt_blocks(torch.from_numpy(p).cuda(), rk, iv)
         torch.cuda.synchronize()
-        assert _lib.last_kernel() == "k_bs_blocks"
+        assert _lib.last_kernel().startswith("k_bs_blocks")
     finally:
         L.gaes_set_variant(0)
     ivrows = np.tile(np.frombuffer(iv, np.uint8), (n, 1))
