@@ -64,6 +64,44 @@ int env_int(const char* name, int dflt) {
 }
 
 // --------------------------------------------------------------------------
+// Host-side parallel byte work (staging copies, shared-IV detection).  Large
+// pageable buffers are copied by several threads: one core's memcpy (~10 GB/s)
+// is slower than a PCIe Gen5 DMA, so a single-threaded staging copy would
+// bound the drop-in path.
+int host_threads() {
+  static int t = [] {
+    int hw = (int)std::thread::hardware_concurrency();
+    int v = env_int("GAES_HOST_THREADS", std::max(1, std::min(8, hw / 2)));
+    return std::max(1, v);
+  }();
+  return t;
+}
+
+template <typename F>
+void parallel_ranges(size_t n, size_t min_per_thread, F&& fn) {
+  const size_t want = std::min<size_t>((size_t)host_threads(), std::max<size_t>(1, n / min_per_thread));
+  if (want <= 1) {
+    fn(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(want - 1);
+  const size_t step = (n + want - 1) / want;
+  for (size_t t = 1; t < want; t++) {
+    const size_t lo = t * step, hi = std::min(n, lo + step);
+    if (lo < hi) th.emplace_back([&fn, lo, hi] { fn(lo, hi); });
+  }
+  fn(0, std::min(n, step));
+  for (auto& x : th) x.join();
+}
+
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  parallel_ranges(bytes, (size_t)4 << 20, [&](size_t lo, size_t hi) {
+    std::memcpy((uint8_t*)dst + lo, (const uint8_t*)src + lo, hi - lo);
+  });
+}
+
+// --------------------------------------------------------------------------
 // Per-device context.
 struct Slot {
   cudaStream_t stream = nullptr;
@@ -86,6 +124,7 @@ struct DevCtx {
   uint32_t* d_std_dec = nullptr;
   uint8_t std_sbox[256], std_inv[256];
   uint32_t std_te[1024], std_td[1024];
+  uint8_t std_mix_fwd[4096], std_mix_inv[4096];  // mix_lut[r][j][x] = M[r][j] * x
   std::mutex cache_mu;
   std::unordered_map<std::string, uint32_t*> cache;  // (box || lut) -> compact tables
   uint8_t* d_scratch = nullptr;  // box(256) lut(4096) perm(16) rk(176)
@@ -158,9 +197,27 @@ int get_ctx(int dev, DevCtx** out) {
   for (int v = 0; v < 256; v++)
     if (c->std_sbox[v] != sbox_forward((uint8_t)v) || c->std_inv[v] != sbox_inverse((uint8_t)v))
       return fail(GAES_ETABLE, "device GF tables disagree with the host field arithmetic");
+  for (int r = 0; r < 4; r++)
+    for (int j = 0; j < 4; j++)
+      for (int x = 0; x < 256; x++) {
+        c->std_mix_fwd[(r * 4 + j) * 256 + x] = gf_mul(mix_coef(false, r, j), (uint8_t)x);
+        c->std_mix_inv[(r * 4 + j) * 256 + x] = gf_mul(mix_coef(true, r, j), (uint8_t)x);
+      }
   *out = c.get();
   g_ctx[dev] = std::move(c);
   return GAES_OK;
+}
+
+// True if the caller's tables equal the device GF layer's (the usual drop-in
+// case: aes_cbc._encrypt_tables / _decrypt_tables build exactly these).
+bool is_standard(const DevCtx* c, bool dec, const uint8_t* box, const uint8_t* lut, const uint8_t* perm);
+
+bool is_standard(const DevCtx* c, bool dec, const uint8_t* box, const uint8_t* lut, const uint8_t* perm) {
+  static const uint8_t kShift[16] = {0, 5, 10, 15, 4, 9, 14, 3, 8, 13, 2, 7, 12, 1, 6, 11};
+  static const uint8_t kInvShift[16] = {0, 13, 10, 7, 4, 1, 14, 11, 8, 5, 2, 15, 12, 9, 6, 3};
+  return std::memcmp(box, dec ? c->std_inv : c->std_sbox, 256) == 0 &&
+         std::memcmp(lut, dec ? c->std_mix_inv : c->std_mix_fwd, 4096) == 0 &&
+         std::memcmp(perm, dec ? kInvShift : kShift, 16) == 0;
 }
 
 int current_ctx(DevCtx** out) {
@@ -351,7 +408,7 @@ int ensure_slot(Slot& s, size_t bytes, size_t iv_bytes, bool staged_in, bool sta
 int finish_slot(Slot& s) {
   GAES_CK(cudaEventSynchronize(s.done));
   if (s.pending_dst) {
-    std::memcpy(s.pending_dst, s.h_out, s.pending_bytes);
+    par_memcpy(s.pending_dst, s.h_out, s.pending_bytes);
     s.pending_dst = nullptr;
     s.pending_bytes = 0;
   }
@@ -451,14 +508,14 @@ int run_job(DevCtx* c, const Job& j) {
     const size_t off = r0 * j.m, bytes = rows * j.m;
     const uint8_t* src = j.data + off;
     if (!in_pinned) {
-      std::memcpy(s.h_in, src, bytes);
+      par_memcpy(s.h_in, src, bytes);
       src = s.h_in;
     }
     GAES_CK(cudaMemcpyAsync(s.d_in, src, bytes, cudaMemcpyHostToDevice, s.stream));
     if (need_iv) {
       const uint8_t* ivsrc = j.ivs + r0 * 16;
       if (!iv_pinned) {
-        std::memcpy(s.h_iv, ivsrc, rows * 16);
+        par_memcpy(s.h_iv, ivsrc, rows * 16);
         ivsrc = s.h_iv;
       }
       GAES_CK(cudaMemcpyAsync(s.d_iv, ivsrc, rows * 16, cudaMemcpyHostToDevice, s.stream));
@@ -537,10 +594,26 @@ int run_sharded(const Job& j) {
   return GAES_OK;
 }
 
+// IVSet.rows tiles a shared IV into N x 16 (aes_cbc.py:107-115); detect it so
+// the IV folds into the key and the grid never crosses PCIe.
 bool rows_share_iv(const uint8_t* ivs, size_t n) {
-  for (size_t i = 1; i < n; i++)
-    if (std::memcmp(ivs, ivs + 16 * i, 16) != 0) return false;
-  return true;
+  std::atomic<bool> same{true};
+  parallel_ranges(n, (size_t)1 << 18, [&](size_t lo, size_t hi) {
+    uint64_t a0, a1;
+    std::memcpy(&a0, ivs, 8);
+    std::memcpy(&a1, ivs + 8, 8);
+    for (size_t i = std::max<size_t>(lo, 1); i < hi; i++) {
+      uint64_t b0, b1;
+      std::memcpy(&b0, ivs + 16 * i, 8);
+      std::memcpy(&b1, ivs + 16 * i + 8, 8);
+      if ((a0 ^ b0) | (a1 ^ b1)) {
+        same.store(false, std::memory_order_relaxed);
+        return;
+      }
+      if ((i & 4095) == 0 && !same.load(std::memory_order_relaxed)) return;
+    }
+  });
+  return same.load();
 }
 
 int check_grid(const void* data, const void* out, size_t n, size_t m) {
@@ -569,7 +642,12 @@ int cbc_host(bool dec, const uint8_t* data, const uint8_t* ivs, size_t n, size_t
   j.lut = lut;
   j.perm = perm;
   j.raw_rk = rk;
-  j.standard = false;
+  {
+    DevCtx* c0 = nullptr;
+    int rc0 = get_ctx(0, &c0);
+    if (rc0) return rc0;
+    j.standard = is_standard(c0, dec, box, lut, perm);
+  }
   if (!std_shift || !linear) {
     j.mode = Mode::kGeneric;
     j.ivs = ivs;
