@@ -114,7 +114,7 @@ struct Slot {
   size_t pending_bytes = 0;
 };
 
-constexpr int kSlots = 3;
+constexpr int kSlots = 4;
 
 struct DevCtx {
   int dev = 0;
@@ -487,13 +487,30 @@ int run_job(DevCtx* c, const Job& j) {
   const bool out_pinned = is_pinned(j.out);
   const bool need_iv = j.ivs != nullptr;
   const bool iv_pinned = need_iv && is_pinned(j.ivs);
-  size_t rows_per_chunk = std::max<size_t>(1, chunk_bytes() / j.m);
-  if (rows_per_chunk > j.n) rows_per_chunk = j.n;
-  const size_t nchunks = (j.n + rows_per_chunk - 1) / rows_per_chunk;
+  // Chunk schedule: ramp up from base/8 so the first H2D is short (nothing
+  // overlaps it), run at `base`, ramp down at the end so the last D2H is
+  // short too.  All chunks are whole rows.
+  const size_t base_rows = std::max<size_t>(1, chunk_bytes() / j.m);
+  const size_t min_rows = std::max<size_t>(1, base_rows / 8);
+  std::vector<std::pair<size_t, size_t>> chunks;  // (first row, rows)
+  {
+    size_t r0 = 0, cur = min_rows;
+    while (r0 < j.n) {
+      const size_t left = j.n - r0;
+      size_t take = std::min(cur, left);
+      if (left <= 2 * base_rows) take = std::min(take, std::max(min_rows, (left + 1) / 2));
+      if (left - take < min_rows / 2) take = left;
+      chunks.emplace_back(r0, take);
+      r0 += take;
+      cur = std::min(base_rows, cur * 2);
+    }
+  }
+  size_t max_rows = 0;
+  for (auto& ch : chunks) max_rows = std::max(max_rows, ch.second);
+  const size_t nchunks = chunks.size();
   const int used_slots = (int)std::min<size_t>(kSlots, nchunks);
   for (int k = 0; k < used_slots; k++) {
-    int rc = ensure_slot(c->slots[k], rows_per_chunk * j.m, need_iv ? rows_per_chunk * 16 : 0, !in_pinned,
-                         !out_pinned);
+    int rc = ensure_slot(c->slots[k], max_rows * j.m, need_iv ? max_rows * 16 : 0, !in_pinned, !out_pinned);
     if (rc) return rc;
   }
   int rc_final = GAES_OK;
@@ -503,8 +520,8 @@ int run_job(DevCtx* c, const Job& j) {
       int rc = finish_slot(s);
       if (rc) return rc;
     }
-    const size_t r0 = ci * rows_per_chunk;
-    const size_t rows = std::min(rows_per_chunk, j.n - r0);
+    const size_t r0 = chunks[ci].first;
+    const size_t rows = chunks[ci].second;
     const size_t off = r0 * j.m, bytes = rows * j.m;
     const uint8_t* src = j.data + off;
     if (!in_pinned) {

@@ -13,6 +13,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "aes_bitslice.cuh"
 #include "aes_ttable.cuh"
 #include "gf.cuh"
@@ -378,9 +382,21 @@ static int grid_for(uint64_t work_items, int per_thread, int sms, int cta_thread
   return (int)ctas;
 }
 
+// The 192 KiB opt-in is set once per (kernel, device); launching small
+// pipeline chunks must not pay a driver call each time.
 template <typename K>
 static cudaError_t set_smem(K kernel) {
-  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
 }
 
 cudaError_t launch_gf_build(uint32_t* enc, uint32_t* dec, uint8_t* sbox, uint8_t* inv, int* err, cudaStream_t s) {
