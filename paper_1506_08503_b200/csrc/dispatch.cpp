@@ -551,10 +551,37 @@ int run_job(DevCtx* c, const Job& j) {
     GAES_CK(cudaMemcpy(sc + 256 + 4096 + 16, j.raw_rk, 176, cudaMemcpyHostToDevice));
   }
 
-  const bool in_pinned = is_pinned(j.data);
-  const bool out_pinned = is_pinned(j.out);
+  bool in_pinned = is_pinned(j.data);
+  bool out_pinned = is_pinned(j.out);
   const bool need_iv = j.ivs != nullptr;
   const bool iv_pinned = need_iv && is_pinned(j.ivs);
+  // Large pageable buffers: page-lock them in place for the call (DMA
+  // straight from/to the caller's memory) instead of staging through the
+  // pinned ring, when GAES_REGISTER_MB (default 64) <= size.
+  struct Registered {
+    std::vector<void*> ptrs;
+    ~Registered() {
+      for (void* p : ptrs) cudaHostUnregister(p);
+    }
+  } registered;
+  {
+    static const size_t reg_min = (size_t)env_int("GAES_REGISTER_MB", 64) << 20;
+    const size_t total = j.n * j.m;
+    if (reg_min > 0 && total >= reg_min) {
+      if (!in_pinned && cudaHostRegister((void*)j.data, total, cudaHostRegisterReadOnly) == cudaSuccess) {
+        registered.ptrs.push_back((void*)j.data);
+        in_pinned = true;
+      } else {
+        cudaGetLastError();
+      }
+      if (!out_pinned && cudaHostRegister((void*)j.out, total, cudaHostRegisterDefault) == cudaSuccess) {
+        registered.ptrs.push_back((void*)j.out);
+        out_pinned = true;
+      } else {
+        cudaGetLastError();
+      }
+    }
+  }
   // Chunk schedule: ramp up from base/8 so the first H2D is short (nothing
   // overlaps it), run at `base`, ramp down at the end so the last D2H is
   // short too.  All chunks are whole rows.
