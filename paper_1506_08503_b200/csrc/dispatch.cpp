@@ -164,7 +164,7 @@ void parallel_ranges(size_t n, size_t min_per_thread, F&& fn) {
 }
 
 void par_memcpy(void* dst, const void* src, size_t bytes) {
-  parallel_ranges(bytes, (size_t)4 << 20, [&](size_t lo, size_t hi) {
+  parallel_ranges(bytes, (size_t)512 << 10, [&](size_t lo, size_t hi) {
     std::memcpy((uint8_t*)dst + lo, (const uint8_t*)src + lo, hi - lo);
   });
 }
@@ -551,41 +551,17 @@ int run_job(DevCtx* c, const Job& j) {
     GAES_CK(cudaMemcpy(sc + 256 + 4096 + 16, j.raw_rk, 176, cudaMemcpyHostToDevice));
   }
 
-  bool in_pinned = is_pinned(j.data);
-  bool out_pinned = is_pinned(j.out);
+  const bool in_pinned = is_pinned(j.data);
+  const bool out_pinned = is_pinned(j.out);
   const bool need_iv = j.ivs != nullptr;
   const bool iv_pinned = need_iv && is_pinned(j.ivs);
-  // Large pageable buffers: page-lock them in place for the call (DMA
-  // straight from/to the caller's memory) instead of staging through the
-  // pinned ring, when GAES_REGISTER_MB (default 64) <= size.
-  struct Registered {
-    std::vector<void*> ptrs;
-    ~Registered() {
-      for (void* p : ptrs) cudaHostUnregister(p);
-    }
-  } registered;
-  {
-    static const size_t reg_min = (size_t)env_int("GAES_REGISTER_MB", 64) << 20;
-    const size_t total = j.n * j.m;
-    if (reg_min > 0 && total >= reg_min) {
-      if (!in_pinned && cudaHostRegister((void*)j.data, total, cudaHostRegisterReadOnly) == cudaSuccess) {
-        registered.ptrs.push_back((void*)j.data);
-        in_pinned = true;
-      } else {
-        cudaGetLastError();
-      }
-      if (!out_pinned && cudaHostRegister((void*)j.out, total, cudaHostRegisterDefault) == cudaSuccess) {
-        registered.ptrs.push_back((void*)j.out);
-        out_pinned = true;
-      } else {
-        cudaGetLastError();
-      }
-    }
-  }
   // Chunk schedule: ramp up from base/8 so the first H2D is short (nothing
   // overlaps it), run at `base`, ramp down at the end so the last D2H is
   // short too.  All chunks are whole rows.
-  const size_t base_rows = std::max<size_t>(1, chunk_bytes() / j.m);
+  // Pageable buffers are staged by host copies: smaller chunks let the copy
+  // of chunk c+1 overlap the DMA of chunk c.
+  const size_t base_bytes = (in_pinned && out_pinned) ? chunk_bytes() : std::min<size_t>(chunk_bytes(), 8u << 20);
+  const size_t base_rows = std::max<size_t>(1, base_bytes / j.m);
   const size_t min_rows = std::max<size_t>(1, base_rows / 8);
   std::vector<std::pair<size_t, size_t>> chunks;  // (first row, rows)
   {
