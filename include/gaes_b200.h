@@ -109,6 +109,15 @@ GAES_API int gaes_encrypt_shared_iv(const uint8_t *data, size_t n, size_t m, con
 GAES_API int gaes_decrypt_shared_iv(const uint8_t *data, size_t n, size_t m, const uint8_t iv[16],
                                     const uint8_t round_keys[176], uint8_t *out);
 
+/* Per-row IV form with the device GF layer's standard tables (no tables
+ * crossing the boundary): ivs u8[n][16]; a shared IV tiled into rows is
+ * detected and folded.  Used by the container path (per-message IVs,
+ * container.py IV mode 0x01). */
+GAES_API int gaes_cbc_encrypt_std(const uint8_t *data, const uint8_t *ivs, size_t n, size_t m,
+                                  const uint8_t round_keys[176], uint8_t *out);
+GAES_API int gaes_cbc_decrypt_std(const uint8_t *data, const uint8_t *ivs, size_t n, size_t m,
+                                  const uint8_t round_keys[176], uint8_t *out);
+
 /* ---- device-resident entry points (stream-ordered, current device) ----
  * Standard tables from the device GF layer.  `iv` is a 16-byte HOST
  * array (shared IV, folded into the round keys) or NULL for a zero IV. */

@@ -73,7 +73,7 @@ int env_int(const char* name, int dflt) {
 int host_threads() {
   static int t = [] {
     int hw = (int)std::thread::hardware_concurrency();
-    int v = env_int("GAES_HOST_THREADS", std::max(1, std::min(8, hw / 2)));
+    int v = env_int("GAES_HOST_THREADS", std::max(1, std::min(12, hw - 4)));
     return std::max(1, v);
   }();
   return t;
@@ -891,6 +891,24 @@ GAES_API int gaes_cbc_decrypt(const uint8_t* data, const uint8_t* ivs, size_t n,
                               const uint8_t round_keys[176], const uint8_t inv_sbox[256],
                               const uint8_t inv_mix_lut[4096], const uint8_t inv_shift_src[16], uint8_t* out) {
   return cbc_host(true, data, ivs, n, m, round_keys, inv_sbox, inv_mix_lut, inv_shift_src, out);
+}
+
+GAES_API int gaes_cbc_encrypt_std(const uint8_t* data, const uint8_t* ivs, size_t n, size_t m,
+                                  const uint8_t round_keys[176], uint8_t* out) {
+  if (n == 0) return GAES_OK;
+  DevCtx* c = nullptr;
+  int rc = get_ctx(0, &c);
+  if (rc) return rc;
+  return cbc_host(false, data, ivs, n, m, round_keys, c->std_sbox, c->std_mix_fwd, kShiftRowsSrc, out);
+}
+
+GAES_API int gaes_cbc_decrypt_std(const uint8_t* data, const uint8_t* ivs, size_t n, size_t m,
+                                  const uint8_t round_keys[176], uint8_t* out) {
+  if (n == 0) return GAES_OK;
+  DevCtx* c = nullptr;
+  int rc = get_ctx(0, &c);
+  if (rc) return rc;
+  return cbc_host(true, data, ivs, n, m, round_keys, c->std_inv, c->std_mix_inv, kInvShiftRowsSrc, out);
 }
 
 GAES_API int gaes_encrypt_shared_iv(const uint8_t* data, size_t n, size_t m, const uint8_t iv[16],

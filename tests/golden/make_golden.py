@@ -118,6 +118,43 @@ def main():
             fx["cfg1_ct_rows_0_64"] = out[:64].copy()
         print(n, digests[str(n)]["sha256_c"])
 
+    # GAES v1 containers (container.py / cli.py paths), test_container.py recipe
+    from gaes import cli, container
+    gkey = bytes.fromhex("000102030405060708090a0b0c0d0e0f")
+    giv = bytes.fromhex("f0e1d2c3b4a5968778695a4b3c2d1e0f")
+    gmsgs = [b"alpha", b"bravo-bravo", b"charlie charlie charlie!"]
+    gb = aes_cbc.pad_zero(gmsgs)
+    gsiv = aes_cbc.IVSet.shared(giv)
+    blob = container.container_bytes(container.CipherContainer(
+        iv_set=gsiv, original_lens=gb.original_lens, payload=aes_cbc.encrypt_batch(gkey, gsiv, gb)))
+    fx["container_golden"] = np.frombuffer(blob, np.uint8).copy()
+    # a records file: newline-separated records of varied lengths
+    rrng = np.random.default_rng(4242)
+    recs = []
+    for _ in range(300):
+        ln = int(rrng.integers(1, 70))
+        r = rrng.integers(0, 256, ln, dtype=np.uint8)
+        r[r == 0x0A] = 0x0B
+        recs.append(r.tobytes())
+    content = b"\n".join(recs) + b"\n"
+    rkey, riv = rrng.bytes(16), rrng.bytes(16)
+    records = cli._split_records(content)
+    rb = aes_cbc.pad_zero(records)
+    rsiv = aes_cbc.IVSet.shared(riv)
+    shared_blob = container.container_bytes(container.CipherContainer(
+        iv_set=rsiv, original_lens=rb.original_lens, payload=aes_cbc.encrypt_batch(rkey, rsiv, rb)))
+    pivs = rrng.integers(0, 256, (rb.n_messages, 16), dtype=np.uint8)
+    rpiv = aes_cbc.IVSet.per_message(pivs)
+    per_blob = container.container_bytes(container.CipherContainer(
+        iv_set=rpiv, original_lens=rb.original_lens, payload=aes_cbc.encrypt_batch(rkey, rpiv, rb)))
+    fx["records_content"] = np.frombuffer(content, np.uint8).copy()
+    fx["records_key"] = np.frombuffer(rkey, np.uint8).copy()
+    fx["records_iv"] = np.frombuffer(riv, np.uint8).copy()
+    fx["records_ivs"] = pivs
+    fx["records_shared_container"] = np.frombuffer(shared_blob, np.uint8).copy()
+    fx["records_permsg_container"] = np.frombuffer(per_blob, np.uint8).copy()
+    digests["container_golden_sha256"] = hashlib.sha256(blob).hexdigest()
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **fx)
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump({"generator": "tests/golden/make_golden.py",

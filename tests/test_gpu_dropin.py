@@ -123,5 +123,10 @@ def test_reference_test_suite_passes_on_cuda_backend():
                         "-p", "no:cacheprovider", "--rootdir", tests_dir, *files],
                        cwd=tests_dir, env=env, capture_output=True, text=True, timeout=900)
     tail = (r.stdout + r.stderr)[-3000:]
+    log_dir = os.path.join(REPO, "gpurun_out")
+    if os.path.isdir(log_dir):  # evidence for the round log (gpurun merges gpurun_out/)
+        with open(os.path.join(log_dir, "reference_suite_on_cuda.log"), "w") as f:
+            f.write(r.stdout[-20000:] + r.stderr[-5000:])
     assert r.returncode == 0, tail
     assert " passed" in tail and "failed" not in tail, tail
+
