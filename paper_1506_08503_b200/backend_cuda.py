@@ -135,3 +135,35 @@ def decrypt_shared_iv(data: np.ndarray, iv: bytes, round_keys, out: np.ndarray |
     if n:
         _lib.check(_lib.lib().gaes_decrypt_shared_iv(_ptr(data), n, m, _ptr(ivb), _ptr(rk), _ptr(out)))
     return out
+
+
+def cbc_encrypt_std(data, ivs, round_keys, out=None) -> np.ndarray:
+    """Per-row-IV encrypt with the device GF layer's standard tables
+    (gaes_cbc_encrypt_std): the encrypt_batch boundary without passing tables."""
+    data = _buf(data, "data", 2)
+    ivs = _buf(np.ascontiguousarray(ivs, np.uint8), "ivs", 2)
+    rk = _buf(np.ascontiguousarray(round_keys, np.uint8).reshape(11, 16), "round_keys", 2)
+    if out is None:
+        out = np.empty_like(data)
+    out = _buf(out, "out", 2, writable=True)
+    n, m = data.shape
+    if ivs.shape != (n, 16) or out.shape != data.shape:
+        raise ValueError("ivs must be N x 16 and out must match data")
+    if n:
+        _lib.check(_lib.lib().gaes_cbc_encrypt_std(_ptr(data), _ptr(ivs), n, m, _ptr(rk), _ptr(out)))
+    return out
+
+
+def cbc_decrypt_std(data, ivs, round_keys, out=None) -> np.ndarray:
+    data = _buf(data, "data", 2)
+    ivs = _buf(np.ascontiguousarray(ivs, np.uint8), "ivs", 2)
+    rk = _buf(np.ascontiguousarray(round_keys, np.uint8).reshape(11, 16), "round_keys", 2)
+    if out is None:
+        out = np.empty_like(data)
+    out = _buf(out, "out", 2, writable=True)
+    n, m = data.shape
+    if ivs.shape != (n, 16) or out.shape != data.shape:
+        raise ValueError("ivs must be N x 16 and out must match data")
+    if n:
+        _lib.check(_lib.lib().gaes_cbc_decrypt_std(_ptr(data), _ptr(ivs), n, m, _ptr(rk), _ptr(out)))
+    return out

@@ -414,3 +414,28 @@ def test_container_golden_recipe():
                              bytes.fromhex("000102030405060708090a0b0c0d0e0f"),
                              iv=bytes.fromhex("f0e1d2c3b4a5968778695a4b3c2d1e0f"))
     assert hashlib.sha256(blob).hexdigest() == "9e8a98b50f59f03773b6990cb07a40b6a2f4e7c0b704e695c6987d3366ea673b"
+
+
+def test_sweep_csv_schema(tmp_path):
+    """Reference CSV schema (bench.py:33-36) with the cuda implementation."""
+    from paper_1506_08503_b200 import sweep
+    out = tmp_path / "s.csv"
+    assert sweep.main(["--kind", "count", "--counts", "1,1000", "--reps", "3", "--out", str(out)]) == 0
+    lines = out.read_text().splitlines()
+    assert lines[0] == ("kind,implementation,n_messages,message_len_bytes,workers,"
+                        "total_bytes,median_seconds,rate_bytes_per_second")
+    assert len(lines) == 3 and lines[1].startswith("count,cuda,1,16,")
+    assert sweep.main(["--kind", "length", "--lengths", "16,100", "--reps", "3", "--device-resident",
+                       "--out", str(out)]) == 0
+    assert out.read_text().splitlines()[2].startswith("length,cuda-device,128,100,")
+
+
+def test_std_entry_points_match_oracle(oracle):
+    rng = np.random.default_rng(21)
+    key = rng.bytes(16)
+    data = rng.integers(0, 256, (333, 48), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (333, 16), dtype=np.uint8)
+    rk = oracle.gen_keys(key)
+    ct = backend_cuda.cbc_encrypt_std(data, ivs, rk)
+    assert np.array_equal(ct, oracle.encrypt(key, ivs, data))
+    assert np.array_equal(backend_cuda.cbc_decrypt_std(ct, ivs, rk), data)
