@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
              const uint4* __restrict__ ivs, uint64_t bpr) {
   extern __shared__ __align__(1024) char smem[];
   fill_tables(smem, compact);
-  const uint32_t lb = (threadIdx.x & 31) * 4;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lb = lane * 4;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
   uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
 
@@ -98,6 +99,19 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
 #pragma unroll
   for (int k = 0; k < ILP; k++)
     if (b + k * T < n_blocks) cur[k] = ld_stream(in + b + k * T);
+
+  // CHAIN mode: (row, j) of every slot is tracked incrementally -- one
+  // 64-bit division per thread instead of one per block.
+  uint64_t row[ILP], jj[ILP], adv_div = 0, adv_mod = 0;
+  if (IVM == kIvChain) {
+#pragma unroll
+    for (int k = 0; k < ILP; k++) {
+      row[k] = (b + k * T) / bpr;
+      jj[k] = (b + k * T) - row[k] * bpr;
+    }
+    adv_div = (ILP * T) / bpr;
+    adv_mod = (ILP * T) - adv_div * bpr;
+  }
 
   while (b < n_blocks) {
     const uint64_t nb = b + ILP * T;
@@ -109,15 +123,25 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
 #pragma unroll
     for (int k = 0; k < ILP; k++) {
       const uint64_t bk = b + k * T;
-      if (bk < n_blocks) {
-        uint4 x = make_uint4(0, 0, 0, 0);
-        if (IVM == kIvChain) {
-          uint64_t j = 0, row = bk;
-          if (bpr != 1) { row = bk / bpr; j = bk - row * bpr; }
-          if (j) x = __ldg(in + bk - 1);
-          else if (ivs) x = __ldg(ivs + row);
+      uint4 x = make_uint4(0, 0, 0, 0);
+      if (IVM == kIvChain) {
+        // The previous ciphertext block is lane-1's current block (lanes
+        // hold consecutive blocks); lane 0 reads it from memory.
+        uint4 prev;
+        prev.x = __shfl_up_sync(0xFFFFFFFFu, cur[k].x, 1);
+        prev.y = __shfl_up_sync(0xFFFFFFFFu, cur[k].y, 1);
+        prev.z = __shfl_up_sync(0xFFFFFFFFu, cur[k].z, 1);
+        prev.w = __shfl_up_sync(0xFFFFFFFFu, cur[k].w, 1);
+        if (bk < n_blocks) {
+          if (jj[k]) x = lane ? prev : __ldg(in + bk - 1);
+          else if (ivs) x = __ldg(ivs + row[k]);
           else x = make_uint4(rk.iv[0], rk.iv[1], rk.iv[2], rk.iv[3]);
         }
+        jj[k] += adv_mod;
+        row[k] += adv_div;
+        if (jj[k] >= bpr) { jj[k] -= bpr; row[k]++; }
+      }
+      if (bk < n_blocks) {
         uint32_t s0 = cur[k].x, s1 = cur[k].y, s2 = cur[k].z, s3 = cur[k].w;
         if (!DEC) {
           s0 ^= rk.w[0] ^ x.x; s1 ^= rk.w[1] ^ x.y; s2 ^= rk.w[2] ^ x.z; s3 ^= rk.w[3] ^ x.w;
@@ -149,9 +173,11 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
     uint4 c = ivs ? __ldg(ivs + row) : make_uint4(rk.iv[0], rk.iv[1], rk.iv[2], rk.iv[3]);
     const uint4* src = in + row * bpr;
     uint4* dst = out + row * bpr;
-    uint4 p = ld_stream(src);
+    // cached loads: lanes walk rows at stride M, so the second 16 B of each
+    // 32-B sector is consumed one iteration later and should hit L1
+    uint4 p = __ldg(src);
     for (uint64_t j = 0; j < bpr; j++) {
-      const uint4 pn = (j + 1 < bpr) ? ld_stream(src + j + 1) : p;
+      const uint4 pn = (j + 1 < bpr) ? __ldg(src + j + 1) : p;
       uint32_t s0 = p.x ^ c.x ^ rk.w[0], s1 = p.y ^ c.y ^ rk.w[1];
       uint32_t s2 = p.z ^ c.z ^ rk.w[2], s3 = p.w ^ c.w ^ rk.w[3];
       encrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
@@ -284,9 +310,15 @@ __global__ void __launch_bounds__(kManyKeyThreads, 1)
   fill_tables(smem, compact);
   const uint32_t lb = (threadIdx.x & 31) * 4;
   const uint64_t n_blocks = bpk * n_keys;
-  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
-  uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= n_blocks) return;
+  // Each CTA owns one contiguous range and its threads stride by blockDim
+  // inside it, so a thread crosses into the next key only at real key
+  // boundaries (grid-wide striding would reload keys on every block when
+  // bpk < grid size).
+  const uint64_t per_cta = ((n_blocks + gridDim.x - 1) / gridDim.x + blockDim.x - 1) / blockDim.x * blockDim.x;
+  const uint64_t lo = (uint64_t)blockIdx.x * per_cta;
+  const uint64_t hi = min(n_blocks, lo + per_cta);
+  uint64_t b = lo + threadIdx.x;
+  if (b >= hi) return;
   uint64_t key = b / bpk;
   uint64_t key_end = (key + 1) * bpk;
   RoundKeys rk;
@@ -301,10 +333,10 @@ __global__ void __launch_bounds__(kManyKeyThreads, 1)
   };
   load_key(key);
   uint4 cur = ld_stream(in + b);
-  while (b < n_blocks) {
-    const uint64_t nb = b + T;
+  while (b < hi) {
+    const uint64_t nb = b + blockDim.x;
     uint4 nxt = cur;
-    if (nb < n_blocks) nxt = ld_stream(in + nb);
+    if (nb < hi) nxt = ld_stream(in + nb);
     if (b >= key_end) {
       key = b / bpk;
       key_end = (key + 1) * bpk;
