@@ -439,3 +439,37 @@ def test_std_entry_points_match_oracle(oracle):
     ct = backend_cuda.cbc_encrypt_std(data, ivs, rk)
     assert np.array_equal(ct, oracle.encrypt(key, ivs, data))
     assert np.array_equal(backend_cuda.cbc_decrypt_std(ct, ivs, rk), data)
+
+
+def test_beyond_4gib_buffers(oracle):
+    """64-bit indexing: > 2^32 bytes per buffer (config 3 is 4 GiB at N=1)."""
+    n = (1 << 28) + 17
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(28)
+    x = torch.randint(0, 256, (n, 16), dtype=torch.uint8, device="cuda", generator=gen)
+    rng = np.random.default_rng(28)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    rk = oracle.gen_keys(key)
+    c = device.encrypt_blocks(x, rk, iv)
+    idx = torch.tensor([0, 1, (1 << 28) - 1, 1 << 28, n - 2, n - 1] + list(range(n - 4096, n - 4000)),
+                       device="cuda")
+    ps, cs = x[idx].cpu().numpy(), c[idx].cpu().numpy()
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (ps.shape[0], 1))
+    assert np.array_equal(cs, oracle.encrypt(key, ivrows, ps))
+    back = device.decrypt_blocks(c, rk, iv, out=c)  # in place
+    assert torch.equal(back, x)
+    del x, c, back
+    torch.cuda.empty_cache()
+
+
+def test_block_cipher_object(oracle):
+    rng = np.random.default_rng(77)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    rk = oracle.gen_keys(key)
+    bc = device.BlockCipher(rk, iv)
+    x = torch.randint(0, 256, (5000, 16), dtype=torch.uint8, device="cuda")
+    c = bc.encrypt(x)
+    assert torch.equal(c, device.encrypt_blocks(x, rk, iv))
+    assert torch.equal(bc.decrypt(c), x)
+    with pytest.raises(ValueError):
+        bc.encrypt(x.view(-1, 32))
