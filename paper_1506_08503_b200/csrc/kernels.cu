@@ -160,7 +160,30 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
   }
 }
 
+// 256-bit global accesses (LDG/STG.E.256 on sm_100a): two consecutive
+// blocks of one row per instruction.
+struct Pair {
+  uint4 a, b;
+};
+__device__ __forceinline__ Pair ld_pair(const uint4* p) {
+  Pair v;
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v.a.x), "=r"(v.a.y), "=r"(v.a.z), "=r"(v.a.w), "=r"(v.b.x), "=r"(v.b.y), "=r"(v.b.z),
+                 "=r"(v.b.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_pair(uint4* p, const uint4& a, const uint4& b) {
+  asm volatile("st.global.cs.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+
 // CBC encrypt along rows: thread per row, serial chain (_kernel.pyx:29-54).
+// Lanes walk 32 different rows (stride M), so every warp access touches 32
+// cache lines; PAIRS moves two blocks per access (32-byte aligned grids),
+// halving the L1 wavefronts per block.
+template <bool PAIRS>
 __global__ void __launch_bounds__(kBlockThreads, 1)
     k_cbc_enc_rows(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_rows, uint64_t bpr,
                    const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
@@ -169,21 +192,43 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
   fill_tables(smem, compact);
   const uint32_t lb = (threadIdx.x & 31) * 4;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  auto enc = [&](const uint4& p, uint4& c) {
+    uint32_t s0 = p.x ^ c.x ^ rk.w[0], s1 = p.y ^ c.y ^ rk.w[1];
+    uint32_t s2 = p.z ^ c.z ^ rk.w[2], s3 = p.w ^ c.w ^ rk.w[3];
+    encrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
+    c = make_uint4(s0, s1, s2, s3);
+  };
   for (uint64_t row = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n_rows; row += T) {
     uint4 c = ivs ? __ldg(ivs + row) : make_uint4(rk.iv[0], rk.iv[1], rk.iv[2], rk.iv[3]);
     const uint4* src = in + row * bpr;
     uint4* dst = out + row * bpr;
-    // cached loads: lanes walk rows at stride M, so the second 16 B of each
-    // 32-B sector is consumed one iteration later and should hit L1
-    uint4 p = __ldg(src);
-    for (uint64_t j = 0; j < bpr; j++) {
-      const uint4 pn = (j + 1 < bpr) ? __ldg(src + j + 1) : p;
-      uint32_t s0 = p.x ^ c.x ^ rk.w[0], s1 = p.y ^ c.y ^ rk.w[1];
-      uint32_t s2 = p.z ^ c.z ^ rk.w[2], s3 = p.w ^ c.w ^ rk.w[3];
-      encrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
-      c = make_uint4(s0, s1, s2, s3);
-      st_stream(dst + j, c);
-      p = pn;
+    if (PAIRS) {
+      const uint64_t pairs = bpr / 2;
+      Pair p = ld_pair(src);
+      for (uint64_t q = 0; q < pairs; q++) {
+        const Pair pn = (q + 1 < pairs) ? ld_pair(src + 2 * q + 2) : p;
+        uint4 c0 = c;
+        enc(p.a, c0);
+        uint4 c1 = c0;
+        enc(p.b, c1);
+        st_pair(dst + 2 * q, c0, c1);
+        c = c1;
+        p = pn;
+      }
+      if (bpr & 1) {  // odd tail block
+        enc(__ldg(src + bpr - 1), c);
+        st_stream(dst + bpr - 1, c);
+      }
+    } else {
+      // cached loads: the second 16 B of each 32-B sector is consumed one
+      // iteration later and should hit L1
+      uint4 p = __ldg(src);
+      for (uint64_t j = 0; j < bpr; j++) {
+        const uint4 pn = (j + 1 < bpr) ? __ldg(src + j + 1) : p;
+        enc(p, c);
+        st_stream(dst + j, c);
+        p = pn;
+      }
     }
   }
 }
@@ -472,11 +517,14 @@ cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* o
 cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint64_t bpr, const uint32_t* compact,
                                 const RoundKeys& rk, const void* ivs, int sms, cudaStream_t s) {
   if (n_rows == 0) return cudaSuccess;
-  cudaError_t e = set_smem(k_cbc_enc_rows);
+  const bool pairs = bpr >= 2 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 31) == 0 &&
+                     (bpr % 2 == 0);
+  auto kern = pairs ? k_cbc_enc_rows<true> : k_cbc_enc_rows<false>;
+  cudaError_t e = set_smem(kern);
   if (e != cudaSuccess) return e;
   const int grid = grid_for(n_rows, 1, sms);
-  k_cbc_enc_rows<<<grid, kBlockThreads, kSmemBytes, s>>>((const uint4*)in, (uint4*)out, n_rows, bpr, compact, rk,
-                                                         (const uint4*)ivs);
+  kern<<<grid, kBlockThreads, kSmemBytes, s>>>((const uint4*)in, (uint4*)out, n_rows, bpr, compact, rk,
+                                               (const uint4*)ivs);
   return cudaGetLastError();
 }
 

@@ -473,3 +473,21 @@ def test_block_cipher_object(oracle):
     assert torch.equal(bc.decrypt(c), x)
     with pytest.raises(ValueError):
         bc.encrypt(x.view(-1, 32))
+
+
+@pytest.mark.parametrize("blocks,offset", [(2, 0), (4, 0), (64, 0), (4, 16), (6, 16)])
+def test_cbc_encrypt_rows_pairs_and_alignment(oracle, blocks, offset):
+    """General-M CBC encrypt: 32-B paired accesses when aligned, 16-B otherwise."""
+    rng = np.random.default_rng(blocks * 10 + offset)
+    key = rng.bytes(16)
+    n = 1500
+    p = rng.integers(0, 256, (n, 16 * blocks), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    rk = oracle.gen_keys(key)
+    flat = torch.zeros(p.size + 64, dtype=torch.uint8, device="cuda")
+    x = flat[offset:offset + p.size].view(n, 16 * blocks)
+    x.copy_(torch.from_numpy(p))
+    oflat = torch.zeros_like(flat)
+    out = oflat[offset:offset + p.size].view(n, 16 * blocks)
+    device.cbc_encrypt(x, rk, torch.from_numpy(ivs).cuda(), out=out)
+    assert np.array_equal(out.cpu().numpy(), oracle.encrypt(key, ivs, p))
