@@ -160,63 +160,6 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
   }
 }
 
-// Small batches (latency-bound, e.g. config 1 = 2^16 blocks): one
-// unreplicated copy of the tables (5 KiB) instead of the 192 KiB lane-
-// replicated layout, so the per-CTA fill is negligible and many small CTAs
-// spread the few blocks over every SM.  Lookups may bank-conflict; at these
-// sizes the launch and the DRAM latency dominate, not the LDS pipe.
-template <bool DEC>
-__global__ void __launch_bounds__(kSmallThreads)
-    k_blocks_small(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks,
-                   const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk) {
-  __shared__ uint32_t t[kCompactWords];
-  for (int i = threadIdx.x; i < kCompactWords; i += blockDim.x) t[i] = __ldg(compact + i);
-  __syncthreads();
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n_blocks; b += stride) {
-    const uint4 v = ld_stream(in + b);
-    uint32_t s0 = v.x, s1 = v.y, s2 = v.z, s3 = v.w;
-#define GAES_T(j, w) t[(j) * 256 + (((w) >> (8 * (j))) & 0xFF)]
-    if (!DEC) {
-      s0 ^= rk.w[0]; s1 ^= rk.w[1]; s2 ^= rk.w[2]; s3 ^= rk.w[3];
-#pragma unroll
-      for (int r = 1; r < 10; r++) {
-        const uint32_t t0 = GAES_T(0, s0) ^ GAES_T(1, s1) ^ GAES_T(2, s2) ^ GAES_T(3, s3) ^ rk.w[4 * r + 0];
-        const uint32_t t1 = GAES_T(0, s1) ^ GAES_T(1, s2) ^ GAES_T(2, s3) ^ GAES_T(3, s0) ^ rk.w[4 * r + 1];
-        const uint32_t t2 = GAES_T(0, s2) ^ GAES_T(1, s3) ^ GAES_T(2, s0) ^ GAES_T(3, s1) ^ rk.w[4 * r + 2];
-        const uint32_t t3 = GAES_T(0, s3) ^ GAES_T(1, s0) ^ GAES_T(2, s1) ^ GAES_T(3, s2) ^ rk.w[4 * r + 3];
-        s0 = t0; s1 = t1; s2 = t2; s3 = t3;
-      }
-    } else {
-      s0 ^= rk.w[40]; s1 ^= rk.w[41]; s2 ^= rk.w[42]; s3 ^= rk.w[43];
-#pragma unroll
-      for (int r = 9; r >= 1; r--) {
-        const uint32_t t0 = GAES_T(0, s0) ^ GAES_T(1, s3) ^ GAES_T(2, s2) ^ GAES_T(3, s1) ^ rk.w[4 * r + 0];
-        const uint32_t t1 = GAES_T(0, s1) ^ GAES_T(1, s0) ^ GAES_T(2, s3) ^ GAES_T(3, s2) ^ rk.w[4 * r + 1];
-        const uint32_t t2 = GAES_T(0, s2) ^ GAES_T(1, s1) ^ GAES_T(2, s0) ^ GAES_T(3, s3) ^ rk.w[4 * r + 2];
-        const uint32_t t3 = GAES_T(0, s3) ^ GAES_T(1, s2) ^ GAES_T(2, s1) ^ GAES_T(3, s0) ^ rk.w[4 * r + 3];
-        s0 = t0; s1 = t1; s2 = t2; s3 = t3;
-      }
-    }
-#undef GAES_T
-#define GAES_S(w, k) (t[4 * 256 + (((w) >> (8 * (k))) & 0xFF)] << (8 * (k)))
-    uint32_t o0, o1, o2, o3;
-    if (!DEC) {
-      o0 = (GAES_S(s0, 0) | GAES_S(s1, 1) | GAES_S(s2, 2) | GAES_S(s3, 3)) ^ rk.w[40];
-      o1 = (GAES_S(s1, 0) | GAES_S(s2, 1) | GAES_S(s3, 2) | GAES_S(s0, 3)) ^ rk.w[41];
-      o2 = (GAES_S(s2, 0) | GAES_S(s3, 1) | GAES_S(s0, 2) | GAES_S(s1, 3)) ^ rk.w[42];
-      o3 = (GAES_S(s3, 0) | GAES_S(s0, 1) | GAES_S(s1, 2) | GAES_S(s2, 3)) ^ rk.w[43];
-    } else {
-      o0 = (GAES_S(s0, 0) | GAES_S(s3, 1) | GAES_S(s2, 2) | GAES_S(s1, 3)) ^ rk.w[0];
-      o1 = (GAES_S(s1, 0) | GAES_S(s0, 1) | GAES_S(s3, 2) | GAES_S(s2, 3)) ^ rk.w[1];
-      o2 = (GAES_S(s2, 0) | GAES_S(s1, 1) | GAES_S(s0, 2) | GAES_S(s3, 3)) ^ rk.w[2];
-      o3 = (GAES_S(s3, 0) | GAES_S(s2, 1) | GAES_S(s1, 2) | GAES_S(s0, 3)) ^ rk.w[3];
-    }
-#undef GAES_S
-    st_stream(out + b, make_uint4(o0, o1, o2, o3));
-  }
-}
-
 // 256-bit global accesses (LDG/STG.E.256 on sm_100a): two consecutive
 // blocks of one row per instruction.
 struct Pair {
@@ -559,19 +502,8 @@ cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* o
                           const uint32_t* compact, const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms,
                           cudaStream_t s) {
   if (n_blocks == 0) return cudaSuccess;
-  if (ivmode == kIvFolded && n_blocks <= kSmallBatchBlocks) {
-    uint64_t ctas = (n_blocks + kSmallThreads - 1) / kSmallThreads;
-    if (ctas > (uint64_t)sms * 8) ctas = (uint64_t)sms * 8;
-    if (dec)
-      k_blocks_small<true><<<(unsigned)ctas, kSmallThreads, 0, s>>>((const uint4*)in, (uint4*)out, n_blocks,
-                                                                     compact, rk);
-    else
-      k_blocks_small<false><<<(unsigned)ctas, kSmallThreads, 0, s>>>((const uint4*)in, (uint4*)out, n_blocks,
-                                                                      compact, rk);
-    return cudaGetLastError();
-  }
-  // Mid-size batches: spread over every SM (one block per thread) rather
-  // than giving few CTAs two blocks per thread; the 192 KiB fill is per CTA.
+  // Small batches: spread over every SM (one block per thread) rather than
+  // giving few CTAs two blocks per thread; the 192 KiB table fill is per CTA.
   if ((uint64_t)sms * kBlockThreads * 8 > n_blocks) ilp = 1;
 #define GAES_CASE(I, D, M) \
   if (ilp == I && dec == D && ivmode == M) return launch_blocks_t<I, D, M>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s);

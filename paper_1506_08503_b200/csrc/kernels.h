@@ -12,8 +12,6 @@ static constexpr int kBlockThreads = 1024;     // k_blocks / k_cbc_enc_rows: 1 C
 static constexpr int kManyKeyThreads = 768;    // k_many_key: 44 round-key registers per thread (<= 85 regs)
 static constexpr int kBsThreads = 128;         // k_bs_blocks: ~170 registers per thread
 static constexpr int kBsCtasPerSm = 3;
-static constexpr int kSmallThreads = 256;        // k_blocks_small
-static constexpr uint64_t kSmallBatchBlocks = 1u << 17;  // below this, the compact-table kernel
 static constexpr int kIvFolded = 0;
 static constexpr int kIvChain = 1;
 
