@@ -328,6 +328,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     if args.variant:
         _lib.check(_lib.lib().gaes_set_variant(args.variant))
+    # one process per GPU: host-buffer calls stay on this rank's device
+    _lib.set_num_gpus(1)
 
     w = WORKLOADS[args.config]
     inp = make_inputs(args.config, rank, world, dev)
@@ -526,6 +528,8 @@ def main():
         "bound": "smem", "kernel": "k_blocks_enc_folded" if args.config != 5 else "k_many_key_enc",
         "achieved": round(lds_achieved, 2), "peak": round(lds_peak, 2), "unit": "Glookup/s",
         "frac": round(lds_achieved / lds_peak, 4), "traffic": traffic,
+        "traffic_unit": "GB per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, profiles/traffic.json)",
+        "algorithmic_gb_per_launch": round(n * HBM_BYTES_PER_BLOCK / 1e9, 4),
         "per_block": f"{LOOKUPS_PER_BLOCK} conflict-free 4-B LDS lookups; peak = {sms} SMs x 32 lanes/clk x "
                      f"{sm_mhz:.0f} MHz (median SM clock sampled during the timed region)",
         "probe_round_rate": round(probe, 2) if probe else None,

@@ -52,7 +52,9 @@ GAES_API const char *gaes_last_error(void);
 GAES_API int gaes_device_count(void);
 /* Number of GPUs the host-buffer entry points shard rows across
  * (contiguous balanced ranges, parallel.py:37-50 semantics).  n <= 0 or
- * n > device count selects all visible devices.  Returns the value set. */
+ * n > device count selects all visible devices (the default).  With one
+ * GPU the caller's current device is used (one process per GPU); with
+ * several, devices 0 .. n-1.  Returns the number now in use. */
 GAES_API int gaes_set_num_gpus(int n);
 GAES_API int gaes_get_num_gpus(void);
 

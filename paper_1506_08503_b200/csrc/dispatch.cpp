@@ -655,8 +655,12 @@ int run_sharded(const Job& j) {
   const int g = gpus_in_use();
   auto chunks = plan_rows(j.n, g);
   std::vector<DevCtx*> ctxs(chunks.size());
+  // One GPU: the caller's current device (one process per GPU under
+  // torchrun).  Several: devices 0 .. g-1 (one process driving the box).
+  int cur = 0;
+  GAES_CK(cudaGetDevice(&cur));
   for (size_t i = 0; i < chunks.size(); i++) {
-    int rc = get_ctx((int)i, &ctxs[i]);
+    int rc = get_ctx(chunks.size() == 1 ? cur : (int)i, &ctxs[i]);
     if (rc) return rc;
   }
   auto shard_job = [&](size_t i) {
@@ -732,7 +736,7 @@ int cbc_host(bool dec, const uint8_t* data, const uint8_t* ivs, size_t n, size_t
   j.raw_rk = rk;
   {
     DevCtx* c0 = nullptr;
-    int rc0 = get_ctx(0, &c0);
+    int rc0 = current_ctx(&c0);
     if (rc0) return rc0;
     j.standard = is_standard(c0, dec, box, lut, perm);
   }
@@ -869,7 +873,7 @@ GAES_API int gaes_tables_are_standard(const uint8_t sbox[256], const uint8_t mix
                                       const uint8_t shift_src[16], int decrypt) {
   if (!sbox || !mix_lut || !shift_src) return fail(GAES_EINVAL, "null table pointer");
   DevCtx* c = nullptr;
-  int rc = get_ctx(0, &c);
+  int rc = current_ctx(&c);
   if (rc) return rc;
   const uint8_t* box = decrypt ? c->std_inv : c->std_sbox;
   if (std::memcmp(box, sbox, 256) != 0) return 0;
@@ -897,7 +901,7 @@ GAES_API int gaes_cbc_encrypt_std(const uint8_t* data, const uint8_t* ivs, size_
                                   const uint8_t round_keys[176], uint8_t* out) {
   if (n == 0) return GAES_OK;
   DevCtx* c = nullptr;
-  int rc = get_ctx(0, &c);
+  int rc = current_ctx(&c);
   if (rc) return rc;
   return cbc_host(false, data, ivs, n, m, round_keys, c->std_sbox, c->std_mix_fwd, kShiftRowsSrc, out);
 }
@@ -906,7 +910,7 @@ GAES_API int gaes_cbc_decrypt_std(const uint8_t* data, const uint8_t* ivs, size_
                                   const uint8_t round_keys[176], uint8_t* out) {
   if (n == 0) return GAES_OK;
   DevCtx* c = nullptr;
-  int rc = get_ctx(0, &c);
+  int rc = current_ctx(&c);
   if (rc) return rc;
   return cbc_host(true, data, ivs, n, m, round_keys, c->std_inv, c->std_mix_inv, kInvShiftRowsSrc, out);
 }
