@@ -146,12 +146,17 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- inputs
 
-def make_inputs(cfg: int, rank: int, world: int, device):
-    """Seeded synthetic plaintext for this rank, generated on the device."""
+def make_inputs(cfg: int, rank: int, world: int, device, blocks: int | None = None):
+    """Seeded synthetic plaintext for this rank, generated on the device.
+
+    ``blocks`` overrides the workload size (tests use small instances of the
+    same generators)."""
     import torch
     from paper_1506_08503_b200.shard import key_slice, rank_slice
 
-    w = WORKLOADS[cfg]
+    w = dict(WORKLOADS[cfg])
+    if blocks is not None:
+        w["blocks"] = blocks
     rng = np.random.default_rng(SEED)
     key, iv = rng.bytes(16), rng.bytes(16)  # bench.py:124-125 draw order
     gen = torch.Generator(device=device)

@@ -491,3 +491,34 @@ def test_cbc_encrypt_rows_pairs_and_alignment(oracle, blocks, offset):
     out = oflat[offset:offset + p.size].view(n, 16 * blocks)
     device.cbc_encrypt(x, rk, torch.from_numpy(ivs).cuda(), out=out)
     assert np.array_equal(out.cpu().numpy(), oracle.encrypt(key, ivs, p))
+
+
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_bench_generators_and_parity(oracle, cfg):
+    """Small instances of the config 3/4/5 generators (bench.make_inputs), encrypted on the GPU."""
+    import bench
+    dev = torch.device("cuda", 0)
+    blocks = {3: 1 << 16, 4: 1 << 16, 5: 1024 * 64}[cfg]
+    inp = bench.make_inputs(cfg, 0, 1, dev, blocks=blocks)
+    p = inp["p"]
+    ph = p.cpu().numpy()
+    if cfg == 3:  # 8 LE int16 samples per block, |x| bounded by the amplitudes + noise
+        s = ph.view(np.int16).reshape(-1)
+        assert s.size == 8 * blocks and np.abs(s.astype(np.int32)).max() <= 32767
+        assert np.abs(s.astype(np.float64)).mean() > 1000  # the sinusoids are there
+    if cfg == 4:  # value in the low 8 bytes, 8 zero bytes, heavy-tailed repeats
+        assert not ph[:, 8:].any()
+        _, counts = np.unique(ph[:, :8], axis=0, return_counts=True)
+        assert counts.max() > 100
+    if cfg == 5:
+        keys, ivs, bpk = inp["keys"], inp["ivs"], inp["bpk"]
+        rk_enc, _ = device.expand_keys(torch.from_numpy(keys).cuda())
+        c = device.many_key_encrypt(p, rk_enc, torch.from_numpy(ivs).cuda()).cpu().numpy()
+        for i in (0, keys.shape[0] - 1):
+            rows = slice(i * bpk, (i + 1) * bpk)
+            assert np.array_equal(c[rows], oracle.encrypt(keys[i].tobytes(), np.tile(ivs[i], (bpk, 1)), ph[rows]))
+        return
+    key, iv = inp["key"], inp["iv"]
+    c = device.encrypt_blocks(p, oracle.gen_keys(key), iv).cpu().numpy()
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (blocks, 1))
+    assert np.array_equal(c, oracle.encrypt(key, ivrows, ph, threads=4))
