@@ -272,10 +272,10 @@ def cpu_baseline(key, iv, budget_s: float):
     t, kind = cpu_reference_rate(key, iv, probe_n, threads, reps=1, warm=1)
     rate = probe_n / max(t[0], 1e-9)
     n = int(min(1 << 26, max(probe_n, rate * budget_s / 2)))
-    times, kind = cpu_reference_rate(key, iv, n, threads, reps=2, warm=0)
+    times, kind = cpu_reference_rate(key, iv, n, threads, reps=4, warm=0)
     sec = statistics.median(times)
     return {"value": n * BYTES_PER_BLOCK / sec / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
-            "sample": f"{n} uniform 16-B blocks (shared IV, seed {SEED + 1}), median of 2 reps, "
+            "sample": f"{n} uniform 16-B blocks (shared IV, seed {SEED + 1}), median of 4 reps, "
                       f"{threads} threads over parallel.plan chunks"}
 
 
