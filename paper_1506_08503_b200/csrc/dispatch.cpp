@@ -196,11 +196,31 @@ struct DevCtx {
   std::mutex cache_mu;
   std::unordered_map<std::string, uint32_t*> cache;  // (box || lut) -> compact tables
   uint8_t* d_scratch = nullptr;  // box(256) lut(4096) perm(16) rk(176)
+  uint8_t* d_tmp = nullptr;      // GF-build outputs + error flag
   Slot slots[kSlots];
+  // Only runs when initialisation fails (live contexts are never destroyed:
+  // freeing after the CUDA runtime has shut down at exit is not allowed).
+  ~DevCtx() {
+    for (void* p : {(void*)d_std_enc, (void*)d_std_dec, (void*)d_scratch, (void*)d_tmp})
+      if (p) cudaFree(p);
+    for (auto& s : slots) {
+      if (s.stream) cudaStreamDestroy(s.stream);
+      if (s.done) cudaEventDestroy(s.done);
+    }
+    for (auto& kv : cache) cudaFree(kv.second);
+  }
+};
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int dev;
+  explicit DeviceGuard(int d) : dev(d) {}
+  ~DeviceGuard() { cudaSetDevice(dev); }
 };
 
 std::mutex g_ctx_mu;
-std::vector<std::unique_ptr<DevCtx>> g_ctx;
+// Contexts live for the process (never destroyed, see ~DevCtx).
+std::vector<DevCtx*>& g_ctx = *new std::vector<DevCtx*>();
 int g_ndev = -1;
 
 int device_count() {
@@ -224,22 +244,22 @@ int get_ctx(int dev, DevCtx** out) {
   if (dev < 0 || dev >= n) return fail(GAES_EINVAL, "device index out of range");
   std::lock_guard<std::mutex> lk(g_ctx_mu);
   if (g_ctx[dev]) {
-    *out = g_ctx[dev].get();
+    *out = g_ctx[dev];
     return GAES_OK;
   }
   auto c = std::make_unique<DevCtx>();
   c->dev = dev;
   int prev = 0;
   GAES_CK(cudaGetDevice(&prev));
+  DeviceGuard guard(prev);
   GAES_CK(cudaSetDevice(dev));
   GAES_CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
   GAES_CK(cudaMalloc(&c->d_std_enc, kCompactWords * 4));
   GAES_CK(cudaMalloc(&c->d_std_dec, kCompactWords * 4));
   GAES_CK(cudaMalloc(&c->d_scratch, 256 + 4096 + 16 + 176 + 512));
-  uint8_t* d_box = nullptr;
-  int* d_err = nullptr;
-  GAES_CK(cudaMalloc(&d_box, 512));
-  GAES_CK(cudaMalloc(&d_err, sizeof(int)));
+  GAES_CK(cudaMalloc(&c->d_tmp, 512 + sizeof(int)));
+  uint8_t* d_box = c->d_tmp;
+  int* d_err = reinterpret_cast<int*>(c->d_tmp + 512);
   GAES_CK(cudaMemset(d_err, 0, sizeof(int)));
   GAES_CK(launch_gf_build(c->d_std_enc, c->d_std_dec, d_box, d_box + 256, d_err, 0));
   note_kernel("k_gf_build");
@@ -252,13 +272,10 @@ int get_ctx(int dev, DevCtx** out) {
   std::memcpy(c->std_te, tmp, sizeof(c->std_te));
   GAES_CK(cudaMemcpy(tmp, c->d_std_dec, sizeof(tmp), cudaMemcpyDeviceToHost));
   std::memcpy(c->std_td, tmp, sizeof(c->std_td));
-  cudaFree(d_box);
-  cudaFree(d_err);
   for (auto& s : c->slots) {
     GAES_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     GAES_CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
   }
-  GAES_CK(cudaSetDevice(prev));
   if (err) return fail(GAES_ETABLE, "GF layer self check failed (S^-1 o S != id or M.M^-1 != I)");
   // The device-built S-box must equal the host restatement of the same
   // field arithmetic (gf.cuh is compiled for both sides).
@@ -271,15 +288,13 @@ int get_ctx(int dev, DevCtx** out) {
         c->std_mix_fwd[(r * 4 + j) * 256 + x] = gf_mul(mix_coef(false, r, j), (uint8_t)x);
         c->std_mix_inv[(r * 4 + j) * 256 + x] = gf_mul(mix_coef(true, r, j), (uint8_t)x);
       }
-  *out = c.get();
-  g_ctx[dev] = std::move(c);
+  g_ctx[dev] = c.release();
+  *out = g_ctx[dev];
   return GAES_OK;
 }
 
 // True if the caller's tables equal the device GF layer's (the usual drop-in
 // case: aes_cbc._encrypt_tables / _decrypt_tables build exactly these).
-bool is_standard(const DevCtx* c, bool dec, const uint8_t* box, const uint8_t* lut, const uint8_t* perm);
-
 bool is_standard(const DevCtx* c, bool dec, const uint8_t* box, const uint8_t* lut, const uint8_t* perm) {
   static const uint8_t kShift[16] = {0, 5, 10, 15, 4, 9, 14, 3, 8, 13, 2, 7, 12, 1, 6, 11};
   static const uint8_t kInvShift[16] = {0, 13, 10, 7, 4, 1, 14, 11, 8, 5, 2, 15, 12, 9, 6, 3};
@@ -527,11 +542,22 @@ int run_job(DevCtx* c, const Job& j) {
   std::lock_guard<std::mutex> lk(c->mu);
   int prev = 0;
   GAES_CK(cudaGetDevice(&prev));
+  DeviceGuard guard(prev);
   GAES_CK(cudaSetDevice(c->dev));
-  struct Restore {
-    int d;
-    ~Restore() { cudaSetDevice(d); }
-  } restore{prev};
+  // On any early return: wait for whatever was issued and drop pending
+  // copy-outs, so the next call never writes into this call's buffers.
+  struct Drain {
+    DevCtx* c;
+    bool armed = true;
+    ~Drain() {
+      if (!armed) return;
+      for (auto& s : c->slots) {
+        if (s.stream) cudaStreamSynchronize(s.stream);
+        s.pending_dst = nullptr;
+        s.pending_bytes = 0;
+      }
+    }
+  } drain{c};
 
   const uint32_t* compact = nullptr;
   if (j.mode != Mode::kGeneric) {
@@ -624,6 +650,7 @@ int run_job(DevCtx* c, const Job& j) {
     int rc = finish_slot(c->slots[ci % kSlots]);
     if (rc && !rc_final) rc_final = rc;
   }
+  drain.armed = rc_final != GAES_OK;
   return rc_final;
 }
 
