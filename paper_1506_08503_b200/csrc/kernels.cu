@@ -8,6 +8,8 @@
 //                     non-linear mix tables (correctness path, still GPU)
 //   k_expand_keys     batched key schedule (key_schedule.py:50-70)
 //   k_many_key        many-key batch (config 5)
+//   k_bs_blocks       bitsliced LOP3 encrypt (variant 2, for comparison)
+//   k_round_probe     roofline probe: the round function without HBM traffic
 //
 // Reference semantics: pkg/src/gaes/_kernel.pyx:12-101.
 #include <cuda_runtime.h>
@@ -345,8 +347,8 @@ __global__ void k_expand_keys(const uint8_t* __restrict__ keys, uint64_t k, cons
 
 // ---------------------------------------------------------------------------
 // Many-key batch: key i owns blocks [i*bpk, (i+1)*bpk).  Round keys live in
-// registers and are reloaded only when a thread's grid-stride walk crosses
-// into the next key's range.
+// registers and are reloaded only when a thread's walk through its CTA's
+// contiguous range crosses into the next key's blocks.
 template <bool DEC>
 __global__ void __launch_bounds__(kManyKeyThreads, 1)
     k_many_key(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t bpk, uint64_t n_keys,
