@@ -329,7 +329,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", 1))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    launched = "RANK" in os.environ and "MASTER_ADDR" in os.environ  # torchrun, any world size
+    if launched:
         dist.init_process_group("nccl", device_id=dev)
     if args.variant:
         _lib.check(_lib.lib().gaes_set_variant(args.variant))
@@ -380,7 +381,7 @@ def main():
         while time.perf_counter() - t_soak < 0.3:
             step()
             torch.cuda.synchronize()
-        if world > 1:
+        if launched:
             dist.barrier()
         torch.cuda.synchronize()
         launches0 = _lib.launch_count()
@@ -394,7 +395,7 @@ def main():
             ends[i].record(stream)
         torch.cuda.synchronize()
         launches = _lib.launch_count() - launches0
-        if world > 1:
+        if launched:
             dist.barrier()
         while time.perf_counter() - t_timed < 0.5:
             step()
@@ -462,7 +463,7 @@ def main():
         hi, ho = h_in.numpy(), h_out.numpy()
         for _ in range(2):
             backend_cuda.encrypt_shared_iv(hi, iv, rk, out=ho)
-        if world > 1:
+        if launched:
             dist.barrier()
         ts = []
         for _ in range(max(3, min(args.steps, 10))):
@@ -565,7 +566,7 @@ def main():
             "decrypt_gbs_per_gpu": round(dec_gbs, 2), "verified": verified,
         }
         print(json.dumps(line))
-    if world > 1:
+    if launched:
         dist.barrier()
         dist.destroy_process_group()
     return 0 if verified else 1
