@@ -223,6 +223,12 @@ std::mutex g_ctx_mu;
 std::vector<DevCtx*>& g_ctx = *new std::vector<DevCtx*>();
 int g_ndev = -1;
 
+// Logical device i -> physical CUDA device g_phys[i].  Identity unless
+// GAES_DEVICE_MAP="a,b,..." is set (e.g. "0,0" runs the multi-GPU shard path
+// as two contexts on one GPU -- used to test the sharding on a 1-GPU box; the
+// shards never wait on each other, so sharing a GPU is safe).
+std::vector<int>& g_phys = *new std::vector<int>();
+
 int device_count() {
   std::lock_guard<std::mutex> lk(g_ctx_mu);
   if (g_ndev < 0) {
@@ -231,8 +237,22 @@ int device_count() {
       cudaGetLastError();
       n = 0;
     }
-    g_ndev = n;
-    g_ctx.resize(n);
+    g_phys.clear();
+    const char* map = std::getenv("GAES_DEVICE_MAP");
+    if (n > 0 && map && *map) {
+      for (const char* p = map; *p;) {
+        char* end = nullptr;
+        const long d = std::strtol(p, &end, 10);
+        if (end == p) break;
+        if (d >= 0 && d < n) g_phys.push_back((int)d);
+        p = (*end == ',') ? end + 1 : end;
+        if (*end != ',' && *end) break;
+      }
+    }
+    if (g_phys.empty())
+      for (int i = 0; i < n; i++) g_phys.push_back(i);
+    g_ndev = (int)g_phys.size();
+    g_ctx.resize(g_ndev);
   }
   return g_ndev;
 }
@@ -248,12 +268,12 @@ int get_ctx(int dev, DevCtx** out) {
     return GAES_OK;
   }
   auto c = std::make_unique<DevCtx>();
-  c->dev = dev;
+  c->dev = g_phys[dev];
   int prev = 0;
   GAES_CK(cudaGetDevice(&prev));
   DeviceGuard guard(prev);
-  GAES_CK(cudaSetDevice(dev));
-  GAES_CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
+  GAES_CK(cudaSetDevice(c->dev));
+  GAES_CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->dev));
   GAES_CK(cudaMalloc(&c->d_std_enc, kCompactWords * 4));
   GAES_CK(cudaMalloc(&c->d_std_dec, kCompactWords * 4));
   GAES_CK(cudaMalloc(&c->d_scratch, 256 + 4096 + 16 + 176 + 512));
@@ -303,11 +323,15 @@ bool is_standard(const DevCtx* c, bool dec, const uint8_t* box, const uint8_t* l
          std::memcmp(perm, dec ? kInvShift : kShift, 16) == 0;
 }
 
+// Context of the caller's current CUDA device (first logical device mapped
+// to it).
 int current_ctx(DevCtx** out) {
   int dev = 0;
   if (device_count() <= 0) return fail(GAES_ENODEV, "no CUDA device visible");
   GAES_CK(cudaGetDevice(&dev));
-  return get_ctx(dev, out);
+  for (size_t i = 0; i < g_phys.size(); i++)
+    if (g_phys[i] == dev) return get_ctx((int)i, out);
+  return fail(GAES_EINVAL, "current device is not in GAES_DEVICE_MAP");
 }
 
 // --------------------------------------------------------------------------
@@ -684,10 +708,8 @@ int run_sharded(const Job& j) {
   std::vector<DevCtx*> ctxs(chunks.size());
   // One GPU: the caller's current device (one process per GPU under
   // torchrun).  Several: devices 0 .. g-1 (one process driving the box).
-  int cur = 0;
-  GAES_CK(cudaGetDevice(&cur));
   for (size_t i = 0; i < chunks.size(); i++) {
-    int rc = get_ctx(chunks.size() == 1 ? cur : (int)i, &ctxs[i]);
+    int rc = chunks.size() == 1 ? current_ctx(&ctxs[i]) : get_ctx((int)i, &ctxs[i]);
     if (rc) return rc;
   }
   auto shard_job = [&](size_t i) {
@@ -858,26 +880,31 @@ GAES_API int gaes_probe_round_rate(int device, uint32_t iters, double* lookups_p
   if (rc) return rc;
   int prev = 0;
   GAES_CK(cudaGetDevice(&prev));
-  GAES_CK(cudaSetDevice(device));
-  uint32_t* sink = nullptr;
-  GAES_CK(cudaMalloc(&sink, 4));
+  DeviceGuard guard(prev);
+  GAES_CK(cudaSetDevice(c->dev));
+  struct Res {
+    uint32_t* sink = nullptr;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ~Res() {
+      if (sink) cudaFree(sink);
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+    }
+  } r;
+  GAES_CK(cudaMalloc(&r.sink, 4));
   uint8_t rk[176] = {0};
   const RoundKeys k = make_enc_keys(rk, nullptr, false);
-  cudaEvent_t a, b;
-  GAES_CK(cudaEventCreate(&a));
-  GAES_CK(cudaEventCreate(&b));
-  GAES_CK(launch_round_probe(c->d_std_enc, k, 16, sink, c->sms, 0));  // warm-up
-  GAES_CK(cudaEventRecord(a, 0));
-  GAES_CK(launch_round_probe(c->d_std_enc, k, iters, sink, c->sms, 0));
-  GAES_CK(cudaEventRecord(b, 0));
-  GAES_CK(cudaEventSynchronize(b));
+  GAES_CK(cudaEventCreate(&r.a));
+  GAES_CK(cudaEventCreate(&r.b));
+  GAES_CK(launch_round_probe(c->d_std_enc, k, 16, r.sink, c->sms, 0));  // warm-up
+  GAES_CK(cudaEventRecord(r.a, 0));
+  GAES_CK(launch_round_probe(c->d_std_enc, k, iters, r.sink, c->sms, 0));
+  GAES_CK(cudaEventRecord(r.b, 0));
+  GAES_CK(cudaEventSynchronize(r.b));
+  note_kernel("k_round_probe");
   note_kernel("k_round_probe");
   float t = 0;
-  GAES_CK(cudaEventElapsedTime(&t, a, b));
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
-  cudaFree(sink);
-  cudaSetDevice(prev);
+  GAES_CK(cudaEventElapsedTime(&t, r.a, r.b));
   const double lookups = (double)c->sms * kBlockThreads * (double)iters * 160.0;
   if (lookups_per_sec) *lookups_per_sec = lookups / (t / 1e3);
   if (ms) *ms = t;

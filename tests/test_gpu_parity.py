@@ -522,3 +522,41 @@ def test_bench_generators_and_parity(oracle, cfg):
     c = device.encrypt_blocks(p, oracle.gen_keys(key), iv).cpu().numpy()
     ivrows = np.tile(np.frombuffer(iv, np.uint8), (blocks, 1))
     assert np.array_equal(c, oracle.encrypt(key, ivrows, ph, threads=4))
+
+
+def test_multi_gpu_shard_path_on_one_gpu(tmp_path):
+    """The in-process multi-GPU dispatcher (plan_rows -> one host thread and
+    context per device) run as two logical devices on one GPU via
+    GAES_DEVICE_MAP=0,0; results must not depend on the shard count
+    (test_parallel.py:55-96 lifted to GPUs)."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, sys
+sys.path.insert(0, ".")
+from oracle import oracle
+from paper_1506_08503_b200 import _lib, backend_cuda
+assert _lib.device_count() == 2, _lib.device_count()
+rng = np.random.default_rng(8)
+key, iv = rng.bytes(16), rng.bytes(16)
+rk = oracle.gen_keys(key)
+for n, m in [(1, 16), (3, 16), (100001, 16), (5003, 48)]:
+    data = rng.integers(0, 256, (n, m), dtype=np.uint8)
+    ivrows = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    want = oracle.encrypt(key, ivrows, data, threads=4)
+    for g in (1, 2):
+        assert _lib.set_num_gpus(g) == g
+        out = np.empty_like(data)
+        backend_cuda.cbc_encrypt(data, ivrows, *oracle.encrypt_tables(key), out)
+        assert np.array_equal(out, want), (n, m, g)
+        back = backend_cuda.cbc_decrypt_std(out, ivrows, rk)
+        assert np.array_equal(back, data), (n, m, g)
+        ct = backend_cuda.encrypt_shared_iv(data, iv, rk)
+        assert np.array_equal(backend_cuda.decrypt_shared_iv(ct, iv, rk), data)
+print("ok")
+'''
+    import os
+    env = dict(os.environ, GAES_DEVICE_MAP="0,0")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
