@@ -543,6 +543,9 @@ def main():
         "algorithmic_gb_per_launch": round(n * HBM_BYTES_PER_BLOCK / 1e9, 4),
         "per_block": f"{LOOKUPS_PER_BLOCK} conflict-free 4-B LDS lookups; peak = {sms} SMs x 32 lanes/clk x "
                      f"{sm_mhz:.0f} MHz (median SM clock sampled during the timed region)",
+        "peak_source": "nominal: 32 conflict-free LDS lanes/clk/SM x SMs x sampled SM clock "
+                       "(MEASURED_PEAKS.json has no shared-memory figure); probe_round_rate = measured "
+                       "ceiling of this formulation on this GPU",
         "probe_round_rate": round(probe, 2) if probe else None,
         "probe_frac": round(lds_achieved / probe, 4) if probe else None,
         "probe_note": "k_round_probe: same round function on register-resident states, no HBM (formulation ceiling)",
