@@ -115,3 +115,14 @@ def test_product_package_does_not_import_the_oracle():
                 text = open(os.path.join(root, f)).read()
                 assert "from oracle" not in text and "import oracle" not in text, f
                 assert "liboracle" not in text and "oracle/_ref" not in text, f
+
+
+def test_c_example_links_against_the_abi(lib, tmp_path):
+    """examples/encrypt_c.c compiles and links with plain gcc (no Python)."""
+    if not shutil.which("gcc"):
+        pytest.skip("no gcc")
+    exe = tmp_path / "encrypt_c"
+    subprocess.check_call(["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(REPO, "include"),
+                           os.path.join(REPO, "examples", "encrypt_c.c"), "-L", os.path.dirname(lib.LIB_PATH),
+                           "-lgaes_b200", f"-Wl,-rpath,{os.path.dirname(lib.LIB_PATH)}", "-o", str(exe)])
+    assert exe.exists()

@@ -560,3 +560,41 @@ print("ok")
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def test_c_example_runs_bit_exact(tmp_path):
+    """The C ABI from C: FIPS-197 C.1 and SP 800-38A through examples/encrypt_c.c."""
+    import os
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("no gcc")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(repo, "paper_1506_08503_b200")
+    exe = tmp_path / "encrypt_c"
+    subprocess.check_call(["gcc", "-O2", "-I", os.path.join(repo, "include"), os.path.join(repo, "examples", "encrypt_c.c"),
+                           "-L", libdir, "-lgaes_b200", f"-Wl,-rpath,{libdir}", "-o", str(exe)])
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
+
+
+try:
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+except ImportError:  # pragma: no cover
+    given = None
+
+if given is not None:
+    @settings(max_examples=60, deadline=None)
+    @given(st.integers(1, 300), st.integers(1, 6), st.booleans(), st.integers(0, 2**32 - 1))
+    def test_property_backend_equals_oracle_and_round_trips(n, blocks, shared, seed):
+        """Hypothesis round trip (test_aes_cbc.py:299-312 style) through the backend contract."""
+        from oracle import oracle
+        rng = np.random.default_rng(seed)
+        key = rng.bytes(16)
+        data = rng.integers(0, 256, (n, 16 * blocks), dtype=np.uint8)
+        ivs = (np.tile(rng.integers(0, 256, 16, dtype=np.uint8), (n, 1)) if shared
+               else rng.integers(0, 256, (n, 16), dtype=np.uint8))
+        ct = _cuda_enc(key, ivs, data, oracle)
+        assert np.array_equal(ct, oracle.encrypt(key, ivs, data))
+        assert np.array_equal(_cuda_dec(key, ivs, ct, oracle), data)
