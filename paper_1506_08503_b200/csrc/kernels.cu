@@ -494,9 +494,7 @@ static cudaError_t launch_blocks_t(const void* in, void* out, uint64_t n, const 
   auto kern = k_blocks<ILP, DEC, IVM>;
   cudaError_t e = set_smem(kern);
   if (e != cudaSuccess) return e;
-  // Spread small batches over every SM: the per-SM lookup work, not the
-  // per-CTA table fill, dominates once a CTA would get > ~64 blocks.
-  const int grid = grid_for((n + 63) / 64, 1, sms, 1);
+  const int grid = grid_for(n, ILP, sms);
   kern<<<grid, kBlockThreads, kSmemBytes, s>>>((const uint4*)in, (uint4*)out, n, compact, rk, (const uint4*)ivs,
                                                bpr);
   return cudaGetLastError();
