@@ -1,12 +1,12 @@
 """Summarise an ncu capture and a launch list into profiles/ (run on the CPU box).
 
-    python scripts/ncu_summary.py <tag> <prof.ncu-rep> <launches.csv> [--blocks N] [--config 2]
+    python scripts/ncu_summary.py <tag> <prof.ncu-rep> [<launches.csv>] [--blocks N] [--config 2]
 
 Writes profiles/<tag>_ncu_summary.md (key counters of the captured kernel),
-profiles/<tag>_launches.csv (our kernels' per-launch device times, cold and
-serialised under ncu -- compare shares, not absolutes) and updates
-profiles/traffic.json (dram read+write bytes per launch, used by bench.py's
-roofline "traffic").
+and, when a launch list is given, profiles/<tag>_launches.csv (per-launch
+device times, cold and serialised under ncu -- compare shares, not
+absolutes) and profiles/traffic.json (dram read+write bytes per launch,
+used by bench.py's roofline "traffic").
 """
 
 from __future__ import annotations
@@ -52,24 +52,11 @@ def raw_metrics(rep: str) -> dict:
     return {h: (v, u) for h, u, v in zip(hdr, units, vals)}, rows[2][hdr.index("Kernel Name")]
 
 
-def stall_reasons(m: dict, top: int = 6):
-    pref = "smsp__average_warp_latency_issue_stalled_"
-    out = []
-    for k, (v, u) in m.items():
-        if k.startswith("smsp__pcsamp_warps_issue_stalled_") and k.endswith(("_not_issued",)) is False:
-            try:
-                out.append((float(v.replace(",", "")), k.replace("smsp__pcsamp_warps_issue_stalled_", "")))
-            except ValueError:
-                pass
-    _ = pref
-    return sorted(out, reverse=True)[:top]
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("tag")
     ap.add_argument("rep")
-    ap.add_argument("launches")
+    ap.add_argument("launches", nargs="?", default=None)
     ap.add_argument("--blocks", type=int, default=1 << 24)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--lookups", type=int, default=160)
@@ -109,6 +96,9 @@ def main():
         f.write("\n".join(lines) + "\n")
 
     # launch list: keep our kernels (and totals for the shares)
+    if a.launches is None:
+        print("\n".join(lines))
+        return
     with open(a.launches) as f:
         text = f.read()
     start = text.index('"ID"')
