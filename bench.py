@@ -479,6 +479,7 @@ def main():
         e2e_blocks = n_e2e * world if w["scaling"] == "weak" else total_blocks
         verified &= bool(np.array_equal(ho[:4096], ch[:4096]))
         e2e = {"value": e2e_blocks * BYTES_PER_BLOCK / e2e_s / 1e9, "unit": "GB/s",
+               "step_ms": [round(t * 1e3, 3) for t in ts],
                "h2d_bytes_per_step": int(n_e2e * 16), "d2h_bytes_per_step": int(n_e2e * 16),
                "api": "backend_cuda.encrypt_shared_iv -> gaes_encrypt_shared_iv (pinned host buffers)"}
 
