@@ -77,6 +77,13 @@ GAES_API int gaes_gf_tables(int device, uint8_t sbox[256], uint8_t inv_sbox[256]
 GAES_API int gaes_tables_are_standard(const uint8_t sbox[256], const uint8_t mix_lut[4096],
                                       const uint8_t shift_src[16], int decrypt);
 
+/* The device GF layer's tables in the reference's backend-argument format
+ * (what aes_cbc._encrypt_tables / _decrypt_tables hand to a backend,
+ * aes_cbc.py:313-342): sbox u8[256] (S or S^-1), mix_lut u8[4][4][256]
+ * (mix_lut[r][j][x] = M[r][j] * x for M = circ(2,3,1,1) or its inverse) and
+ * shift_src u8[16].  Any pointer may be NULL. */
+GAES_API int gaes_std_tables(int decrypt, uint8_t sbox[256], uint8_t mix_lut[4096], uint8_t shift_src[16]);
+
 /* ---- reference backend contract (host buffers, synchronous) ----------
  * Replaces _kernel.cbc_encrypt (pkg/src/gaes/_kernel.pyx:12-54) and
  * _kernel_np.cbc_encrypt (_kernel_np.py:34-48).

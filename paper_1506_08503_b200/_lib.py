@@ -32,6 +32,7 @@ SIGNATURES = {
     "gaes_get_num_gpus": (_i, []),
     "gaes_gf_tables": (_i, [_i, _vp, _vp, _vp, _vp]),
     "gaes_tables_are_standard": (_i, [_vp, _vp, _vp, _i]),
+    "gaes_std_tables": (_i, [_i, _vp, _vp, _vp]),
     "gaes_cbc_encrypt": (_i, [_vp, _vp, _sz, _sz, _vp, _vp, _vp, _vp, _vp]),
     "gaes_cbc_decrypt": (_i, [_vp, _vp, _sz, _sz, _vp, _vp, _vp, _vp, _vp]),
     "gaes_cbc_encrypt_std": (_i, [_vp, _vp, _sz, _sz, _vp, _vp]),

@@ -167,3 +167,13 @@ def cbc_decrypt_std(data, ivs, round_keys, out=None) -> np.ndarray:
     if n:
         _lib.check(_lib.lib().gaes_cbc_decrypt_std(_ptr(data), _ptr(ivs), n, m, _ptr(rk), _ptr(out)))
     return out
+
+
+def standard_tables(decrypt: bool = False):
+    """(sbox, mix_lut, shift_src) from the device GF layer, in the format
+    aes_cbc._encrypt_tables / _decrypt_tables pass to a backend."""
+    box = np.empty(256, np.uint8)
+    lut = np.empty((4, 4, 256), np.uint8)
+    perm = np.empty(16, np.uint8)
+    _lib.check(_lib.lib().gaes_std_tables(int(bool(decrypt)), _ptr(box), _ptr(lut), _ptr(perm)))
+    return box, lut, perm

@@ -924,6 +924,16 @@ GAES_API int gaes_gf_tables(int device, uint8_t sbox[256], uint8_t inv_sbox[256]
   return GAES_OK;
 }
 
+GAES_API int gaes_std_tables(int decrypt, uint8_t sbox[256], uint8_t mix_lut[4096], uint8_t shift_src[16]) {
+  DevCtx* c = nullptr;
+  int rc = current_ctx(&c);
+  if (rc) return rc;
+  if (sbox) std::memcpy(sbox, decrypt ? c->std_inv : c->std_sbox, 256);
+  if (mix_lut) std::memcpy(mix_lut, decrypt ? c->std_mix_inv : c->std_mix_fwd, 4096);
+  if (shift_src) std::memcpy(shift_src, decrypt ? kInvShiftRowsSrc : kShiftRowsSrc, 16);
+  return GAES_OK;
+}
+
 GAES_API int gaes_tables_are_standard(const uint8_t sbox[256], const uint8_t mix_lut[4096],
                                       const uint8_t shift_src[16], int decrypt) {
   if (!sbox || !mix_lut || !shift_src) return fail(GAES_EINVAL, "null table pointer");

@@ -598,3 +598,12 @@ if given is not None:
         ct = _cuda_enc(key, ivs, data, oracle)
         assert np.array_equal(ct, oracle.encrypt(key, ivs, data))
         assert np.array_equal(_cuda_dec(key, ivs, ct, oracle), data)
+
+
+def test_standard_tables_equal_reference_tables(golden):
+    box, lut, perm = backend_cuda.standard_tables(False)
+    assert np.array_equal(box, golden["sbox"]) and np.array_equal(lut, golden["mix_fwd"])
+    assert np.array_equal(perm, golden["shift"])
+    box, lut, perm = backend_cuda.standard_tables(True)
+    assert np.array_equal(box, golden["inv_sbox"]) and np.array_equal(lut, golden["mix_inv"])
+    assert np.array_equal(perm, golden["inv_shift"])
