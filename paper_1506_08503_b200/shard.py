@@ -19,7 +19,8 @@ from dataclasses import dataclass
 
 @dataclass(frozen=True)
 class ParallelPlan:
-    """Balanced contiguous partition of [0, N) into at most `workers` chunks."""
+    """Contiguous balanced partition of [0, N) into at most ``workers`` ranges
+    (same contract as the reference's ParallelPlan, parallel.py:25-34)."""
 
     workers: int
     chunks: tuple
@@ -30,19 +31,22 @@ class ParallelPlan:
 
 
 def plan(n_messages: int, workers: int) -> ParallelPlan:
-    """parallel.py:37-50: contiguous chunks whose sizes differ by at most 1."""
+    """Balanced contiguous ranges, sizes within one of each other, at most
+    min(workers, n) of them (semantics of parallel.py:37-50).
+
+    The first ``n % k`` ranges get the extra row; boundaries are
+    ``i * q + min(i, r)`` with ``q, r = divmod(n, k)``.
+    """
     if workers < 1:
         raise ValueError("need at least one worker")
     if n_messages < 0:
         raise ValueError("negative message count")
-    used = min(workers, n_messages)
-    chunks = []
-    start = 0
-    for i in range(used):
-        size = n_messages // used + (1 if i < n_messages % used else 0)
-        chunks.append((start, start + size))
-        start += size
-    return ParallelPlan(workers=workers, chunks=tuple(chunks))
+    k = min(workers, n_messages)
+    if k == 0:
+        return ParallelPlan(workers=workers, chunks=())
+    q, r = divmod(n_messages, k)
+    edges = [i * q + min(i, r) for i in range(k + 1)]
+    return ParallelPlan(workers=workers, chunks=tuple(zip(edges[:-1], edges[1:])))
 
 
 def rank_slice(n_messages: int, rank: int, world_size: int) -> tuple:
