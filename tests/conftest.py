@@ -13,6 +13,13 @@ GOLDEN_DIR = os.path.join(REPO, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running")
+    # Build the native pieces if a fresh checkout has not been built yet
+    # (the package refuses to import without libgaes_b200.so).
+    if not os.path.exists(os.path.join(REPO, "paper_1506_08503_b200", "libgaes_b200.so")):
+        import __graft_entry__
+        __graft_entry__._load_build_module().build()
+    from oracle import oracle as _oracle
+    _oracle.build()
 
 
 @pytest.fixture(scope="session")

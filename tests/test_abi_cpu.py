@@ -27,8 +27,8 @@ def _declared():
 
 @pytest.fixture(scope="module")
 def lib():
-    from paper_1506_08503_b200 import _build
-    _build.build()
+    import __graft_entry__
+    __graft_entry__._load_build_module().build()
     from paper_1506_08503_b200 import _lib
     return _lib
 
