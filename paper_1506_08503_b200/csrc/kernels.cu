@@ -91,7 +91,13 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
              const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
              const uint4* __restrict__ ivs, uint64_t bpr) {
   extern __shared__ __align__(1024) char smem[];
+  // Programmatic dependent launch: let the next launch on this stream start
+  // its CTAs (and their table fill) as SMs free up, and wait for the
+  // previous launch's memory only after our own fill.  No-ops when the
+  // launch carries no PDL attribute.
+  asm volatile("griddepcontrol.launch_dependents;");
   fill_tables(smem, compact);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lb = lane * 4;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
@@ -495,9 +501,17 @@ static cudaError_t launch_blocks_t(const void* in, void* out, uint64_t n, const 
   cudaError_t e = set_smem(kern);
   if (e != cudaSuccess) return e;
   const int grid = grid_for(n, ILP, sms);
-  kern<<<grid, kBlockThreads, kSmemBytes, s>>>((const uint4*)in, (uint4*)out, n, compact, rk, (const uint4*)ivs,
-                                               bpr);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kBlockThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, (const uint4*)in, (uint4*)out, n, compact, rk, (const uint4*)ivs, bpr);
 }
 
 cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* out, uint64_t n_blocks,
