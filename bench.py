@@ -397,12 +397,22 @@ def main():
         # exactly K steps.
         step()
         launches0 = _lib.launch_count()
-        for i in range(args.steps):
-            if flush is not None:
+        if flush is not None:
+            # small working set: flush L2 between steps, each step bracketed
+            # by its own events (the flush is outside them)
+            for i in range(args.steps):
                 flush.fill_(i & 0xFF)
-            starts[i].record(stream)
-            step()
-            ends[i].record(stream)
+                starts[i].record(stream)
+                step()
+                ends[i].record(stream)
+        else:
+            # inputs larger than L2: the K steps run back to back between one
+            # pair of events (no event between launches, so a launch can
+            # start its CTAs while the previous one drains)
+            starts[0].record(stream)
+            for i in range(args.steps):
+                step()
+            ends[0].record(stream)
         torch.cuda.synchronize()
         launches = _lib.launch_count() - launches0
         if launched:
@@ -415,7 +425,10 @@ def main():
     clocks["window"] = "timed region + same-kernel soak to >= 0.5 s"
     clocks["throttled"] = any(r in clocks["reasons"] for r in
                               ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"))
-    ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    if flush is not None:
+        ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    else:
+        ms = [starts[0].elapsed_time(ends[0]) / args.steps] * args.steps
     ms_local = sum(ms) / len(ms)
     ms_step = max_over_ranks(ms_local, dev)
     total_blocks = n * world if w["scaling"] == "weak" else w["blocks"]
