@@ -484,17 +484,27 @@ def main():
     for _ in range(3):
         dstep()
     torch.cuda.synchronize()
-    dms = []
-    for _ in range(max(3, min(args.steps, 10))):
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if flush is not None:
+    dreps = max(3, min(args.steps, 10))
+    if flush is not None:
+        dms = []
+        for _ in range(dreps):
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             flush.fill_(7)
-        ev0.record(stream)
+            ev0.record(stream)
+            dstep()
+            ev1.record(stream)
+            dms.append((ev0, ev1))
+        torch.cuda.synchronize()
+        dec_ms = sum(a.elapsed_time(b) for a, b in dms) / len(dms)
+    else:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         dstep()
+        ev0.record(stream)
+        for _ in range(dreps):
+            dstep()
         ev1.record(stream)
-        dms.append((ev0, ev1))
-    torch.cuda.synchronize()
-    dec_ms = sum(a.elapsed_time(b) for a, b in dms) / len(dms)
+        torch.cuda.synchronize()
+        dec_ms = ev0.elapsed_time(ev1) / dreps
     dec_gbs = n * BYTES_PER_BLOCK / (dec_ms / 1e3) / 1e9
 
     # ---- e2e through the public host-buffer API (pinned host memory)
