@@ -74,6 +74,17 @@ __global__ void k_build_tables(const uint8_t* __restrict__ box, const uint8_t* _
 }
 
 // ---------------------------------------------------------------------------
+// Kernel prologue for launches with programmatic dependent launch: allow the
+// next launch on the stream to start its CTAs as SMs free up, fill our
+// tables, then wait for the previous launch's memory before any global
+// access to data.  griddepcontrol.* are no-ops without the PDL attribute.
+__device__ __forceinline__ void pdl_prologue(char* smem, const uint32_t* __restrict__ compact) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  fill_tables(smem, compact);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
 // Streaming 16-byte loads/stores (data is touched exactly once).
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(uint4* p, uint4 v) { __stcs(p, v); }
@@ -91,13 +102,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
              const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
              const uint4* __restrict__ ivs, uint64_t bpr) {
   extern __shared__ __align__(1024) char smem[];
-  // Programmatic dependent launch: let the next launch on this stream start
-  // its CTAs (and their table fill) as SMs free up, and wait for the
-  // previous launch's memory only after our own fill.  No-ops when the
-  // launch carries no PDL attribute.
-  asm volatile("griddepcontrol.launch_dependents;");
-  fill_tables(smem, compact);
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  pdl_prologue(smem, compact);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lb = lane * 4;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
                    const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
                    const uint4* __restrict__ ivs) {
   extern __shared__ __align__(1024) char smem[];
-  fill_tables(smem, compact);
+  pdl_prologue(smem, compact);
   const uint32_t lb = (threadIdx.x & 31) * 4;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
   auto enc = [&](const uint4& p, uint4& c) {
@@ -360,7 +365,7 @@ __global__ void __launch_bounds__(kManyKeyThreads, 1)
     k_many_key(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t bpk, uint64_t n_keys,
                const uint32_t* __restrict__ compact, const uint4* __restrict__ rks, const uint4* __restrict__ ivs) {
   extern __shared__ __align__(1024) char smem[];
-  fill_tables(smem, compact);
+  pdl_prologue(smem, compact);
   const uint32_t lb = (threadIdx.x & 31) * 4;
   const uint64_t n_blocks = bpk * n_keys;
   // Each CTA owns one contiguous range and its threads stride by blockDim
@@ -467,6 +472,26 @@ static int grid_for(uint64_t work_items, int per_thread, int sms, int cta_thread
   return (int)ctas;
 }
 
+// Launch with programmatic stream serialization allowed (PDL): the kernel
+// may start its CTAs -- and their 192 KiB table fill -- while the previous
+// launch on the stream drains; it waits (griddepcontrol.wait) before
+// touching global data.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // The 192 KiB opt-in is set once per (kernel, device); launching small
 // pipeline chunks must not pay a driver call each time.
 template <typename K>
@@ -501,17 +526,8 @@ static cudaError_t launch_blocks_t(const void* in, void* out, uint64_t n, const 
   cudaError_t e = set_smem(kern);
   if (e != cudaSuccess) return e;
   const int grid = grid_for(n, ILP, sms);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kBlockThreads);
-  cfg.dynamicSmemBytes = kSmemBytes;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, (const uint4*)in, (uint4*)out, n, compact, rk, (const uint4*)ivs, bpr);
+  return launch_pdl(kern, grid, kBlockThreads, kSmemBytes, s, (const uint4*)in, (uint4*)out, n, compact, rk,
+                    (const uint4*)ivs, bpr);
 }
 
 cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* out, uint64_t n_blocks,
@@ -539,9 +555,8 @@ cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint
   cudaError_t e = set_smem(kern);
   if (e != cudaSuccess) return e;
   const int grid = grid_for(n_rows, 1, sms);
-  kern<<<grid, kBlockThreads, kSmemBytes, s>>>((const uint4*)in, (uint4*)out, n_rows, bpr, compact, rk,
-                                               (const uint4*)ivs);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, kBlockThreads, kSmemBytes, s, (const uint4*)in, (uint4*)out, n_rows, bpr, compact,
+                    rk, (const uint4*)ivs);
 }
 
 cudaError_t launch_generic(bool dec, const uint8_t* data, const uint8_t* ivs, uint64_t n, uint64_t m,
@@ -592,13 +607,8 @@ cudaError_t launch_many_key(bool dec, const void* in, void* out, uint64_t bpk, u
   cudaError_t e = dec ? set_smem(k_many_key<true>) : set_smem(k_many_key<false>);
   if (e != cudaSuccess) return e;
   const int grid = grid_for(bpk * n_keys, 1, sms, kManyKeyThreads);
-  if (dec)
-    k_many_key<true><<<grid, kManyKeyThreads, kSmemBytes, s>>>((const uint4*)in, (uint4*)out, bpk, n_keys, compact,
-                                                             (const uint4*)rks, (const uint4*)ivs);
-  else
-    k_many_key<false><<<grid, kManyKeyThreads, kSmemBytes, s>>>((const uint4*)in, (uint4*)out, bpk, n_keys, compact,
-                                                              (const uint4*)rks, (const uint4*)ivs);
-  return cudaGetLastError();
+  return launch_pdl(dec ? k_many_key<true> : k_many_key<false>, grid, kManyKeyThreads, kSmemBytes, s,
+                    (const uint4*)in, (uint4*)out, bpk, n_keys, compact, (const uint4*)rks, (const uint4*)ivs);
 }
 
 }  // namespace gaes
