@@ -2,7 +2,7 @@
 pipelines with torch streams (same shape as the library's host pipeline),
 varying chunk size / stream count / kernel on-off."""
 import sys, time
-import numpy as np, torch
+import torch
 sys.path.insert(0, ".")
 from paper_1506_08503_b200 import device, backend_cuda
 
