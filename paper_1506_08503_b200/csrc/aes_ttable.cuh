@@ -37,17 +37,27 @@ __device__ __forceinline__ uint32_t taddr(uint32_t s, uint32_t lanebase) {
   return __byte_perm(s, lanebase, 0x5504 | (K << 4));
 }
 
-// Replicate the compact tables into the CTA's shared memory.
+// Word i of the compact tables, staged in the unused upper half of region 2
+// (the S region only uses words 0..31 of each 256-byte entry).
+__device__ __forceinline__ uint32_t* stage_word(char* smem, int i) {
+  return reinterpret_cast<uint32_t*>(smem + kOffS + (i >> 5) * 256 + 128 + (i & 31) * 4);
+}
+
+// Replicate the compact tables into the CTA's shared memory.  Two phases:
+// one coalesced pass brings the 5 KiB compact set from L2 into smem (a
+// single L2 round trip per thread), then smem-to-smem replication.  Reading
+// L2 inside the replication loop made every thread wait ~10 dependent L2
+// round trips (~8 us per launch).
 __device__ __forceinline__ void fill_tables(char* smem, const uint32_t* __restrict__ compact) {
-  // 3 regions x 256 entries x 2 halves x 8 uint4 per half
-  for (int q = threadIdx.x; q < 3 * 256 * 2 * 8; q += blockDim.x) {
+  for (int i = threadIdx.x; i < kCompactWords; i += blockDim.x) *stage_word(smem, i) = __ldg(compact + i);
+  __syncthreads();
+  // 5 tables x 256 entries x 8 uint4 (32 lane copies) per entry
+  for (int q = threadIdx.x; q < 5 * 256 * 8; q += blockDim.x) {
     const int quad = q & 7;
-    const int half = (q >> 3) & 1;
-    const int x = (q >> 4) & 255;
-    const int region = q >> 12;
-    const int tbl = region * 2 + half;
-    const uint32_t v = tbl < 5 ? __ldg(compact + tbl * 256 + x) : 0u;
-    *reinterpret_cast<uint4*>(smem + region * kRegionBytes + x * 256 + half * 128 + quad * 16) =
+    const int x = (q >> 3) & 255;
+    const int tbl = q >> 11;
+    const uint32_t v = *stage_word(smem, tbl * 256 + x);
+    *reinterpret_cast<uint4*>(smem + (tbl >> 1) * kRegionBytes + x * 256 + (tbl & 1) * 128 + quad * 16) =
         make_uint4(v, v, v, v);
   }
   __syncthreads();
