@@ -39,3 +39,18 @@ def timed(with_flush, reps=20, back_to_back=False):
 print(f"per-step events, L2 flushed between: {timed(True):.2f} us")
 print(f"per-step events, no flush:           {timed(False):.2f} us")
 print(f"back to back (PDL), no flush:        {timed(False, back_to_back=True):.2f} us")
+
+import ctypes
+from paper_1506_08503_b200 import _lib
+r, m = ctypes.c_double(), ctypes.c_double()
+for it in (0, 1, 4):
+    _lib.check(_lib.lib().gaes_probe_round_rate(0, it, ctypes.addressof(r), ctypes.addressof(m)))
+    print(f"round probe (148 CTAs x 1024 thr, 192 KiB fill, {it} encryptions/thread): {m.value * 1e3:.2f} us")
+e = torch.empty(1, device="cuda")
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record(s)
+for _ in range(100):
+    e.add_(1)
+b.record(s)
+torch.cuda.synchronize()
+print(f"tiny torch kernel back to back: {a.elapsed_time(b) / 100 * 1e3:.2f} us")
