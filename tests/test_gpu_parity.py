@@ -607,3 +607,50 @@ def test_standard_tables_equal_reference_tables(golden):
     box, lut, perm = backend_cuda.standard_tables(True)
     assert np.array_equal(box, golden["inv_sbox"]) and np.array_equal(lut, golden["mix_inv"])
     assert np.array_equal(perm, golden["inv_shift"])
+
+
+def test_device_api_argument_errors(oracle):
+    rk = oracle.gen_keys(bytes(16))
+    x = torch.zeros((64, 16), dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError):
+        device.encrypt_blocks(x.cpu(), rk)                      # host tensor
+    with pytest.raises(ValueError):
+        device.encrypt_blocks(x.to(torch.int16), rk)            # dtype
+    with pytest.raises(ValueError):
+        device.encrypt_blocks(x.t(), rk)                        # non-contiguous
+    with pytest.raises(ValueError):
+        device.encrypt_blocks(x, rk[:10])                       # short schedule
+    with pytest.raises(ValueError):
+        device.cbc_encrypt(torch.zeros((4, 20), dtype=torch.uint8, device="cuda"), rk)
+    with pytest.raises(ValueError):
+        device.many_key_encrypt(x, torch.zeros((3, 11, 16), dtype=torch.uint8, device="cuda"))  # 64 % 3
+    L = _lib.lib()
+    assert L.gaes_encrypt_blocks_dev(None, None, 5, None, None, None) == _lib.GAES_EINVAL
+    assert b"null" in L.gaes_last_error()
+    assert L.gaes_encrypt_blocks_dev(None, None, 0, None, None, None) == 0  # n == 0 no-op
+    with pytest.raises(ValueError):
+        _lib.check(L.gaes_gf_tables(99, None, None, None, None))
+    assert L.gaes_set_variant(7) == _lib.GAES_EINVAL
+
+
+def test_concurrent_device_api_on_streams(oracle):
+    """Device entry points are stream-ordered and re-entrant across host threads."""
+    rng = np.random.default_rng(31)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    rk = oracle.gen_keys(key)
+    xs = [torch.from_numpy(rng.integers(0, 256, (70000, 16), dtype=np.uint8)).cuda() for _ in range(4)]
+    outs = [None] * 4
+
+    def work(i):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            outs[i] = device.encrypt_blocks(xs[i], rk, iv)
+        s.synchronize()
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    for i in range(4):
+        assert torch.equal(outs[i], device.encrypt_blocks(xs[i], rk, iv))
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (1000, 1))
+    assert np.array_equal(outs[0][:1000].cpu().numpy(), oracle.encrypt(key, ivrows, xs[0][:1000].cpu().numpy()))
