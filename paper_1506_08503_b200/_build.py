@@ -16,7 +16,7 @@ REPO = os.path.dirname(PKG_DIR)
 CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_PATH = os.path.join(PKG_DIR, "libgaes_b200.so")
 SOURCES = ["kernels.cu", "dispatch.cpp"]
-HEADERS = ["gf.cuh", "aes_ttable.cuh", "kernels.h"]
+HEADERS = ["gf.cuh", "aes_ttable.cuh", "aes_bitslice.cuh", "kernels.h", "types.h", "host_pool.h", "round_keys.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                      "-Xptxas", "-O3", "-I", os.path.join(REPO, "include")]

@@ -25,9 +25,12 @@
 #include "../../include/gaes_b200.h"
 #include "aes_bitslice.cuh"
 #include "gf.cuh"
+#include "host_pool.h"
 #include "kernels.h"
+#include "round_keys.h"
 
 using namespace gaes;
+using namespace gaes::host;
 
 namespace {
 
@@ -63,110 +66,6 @@ int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   if (!v || !*v) return dflt;
   return std::atoi(v);
-}
-
-// --------------------------------------------------------------------------
-// Host-side parallel byte work (staging copies, shared-IV detection).  Large
-// pageable buffers are copied by several threads: one core's memcpy (~10 GB/s)
-// is slower than a PCIe Gen5 DMA, so a single-threaded staging copy would
-// bound the drop-in path.
-int host_threads() {
-  static int t = [] {
-    int hw = (int)std::thread::hardware_concurrency();
-    int v = env_int("GAES_HOST_THREADS", std::max(1, std::min(12, hw - 4)));
-    return std::max(1, v);
-  }();
-  return t;
-}
-
-// Persistent workers (spawning threads per staging copy costs ~50 us).
-class HostPool {
- public:
-  explicit HostPool(int n) {
-    for (int i = 0; i < n; i++) workers_.emplace_back([this] { loop(); });
-  }
-  ~HostPool() {
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
-    }
-    cv_.notify_all();
-    for (auto& w : workers_) w.join();
-  }
-  // Runs fn(i) for i in [0, parts) on the workers plus the calling thread.
-  void run(size_t parts, const std::function<void(size_t)>& fn) {
-    std::unique_lock<std::mutex> call(call_mu_);  // one parallel region at a time
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      fn_ = &fn;
-      parts_ = parts;
-      next_.store(0);
-      pending_ = parts;
-      gen_++;
-    }
-    cv_.notify_all();
-    work();
-    std::unique_lock<std::mutex> lk(mu_);
-    done_cv_.wait(lk, [this] { return pending_ == 0; });
-    fn_ = nullptr;
-  }
-
- private:
-  void work() {
-    for (;;) {
-      const size_t i = next_.fetch_add(1);
-      if (i >= parts_) return;
-      (*fn_)(i);
-      std::lock_guard<std::mutex> lk(mu_);
-      if (--pending_ == 0) done_cv_.notify_all();
-    }
-  }
-  void loop() {
-    uint64_t seen = 0;
-    for (;;) {
-      {
-        std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return stop_ || (gen_ != seen && fn_ != nullptr); });
-        if (stop_) return;
-        seen = gen_;
-      }
-      work();
-    }
-  }
-  std::vector<std::thread> workers_;
-  std::mutex mu_, call_mu_;
-  std::condition_variable cv_, done_cv_;
-  const std::function<void(size_t)>* fn_ = nullptr;
-  size_t parts_ = 0, pending_ = 0;
-  std::atomic<size_t> next_{0};
-  uint64_t gen_ = 0;
-  bool stop_ = false;
-};
-
-HostPool& host_pool() {
-  static HostPool* pool = new HostPool(std::max(0, host_threads() - 1));  // leaked: lives until exit
-  return *pool;
-}
-
-template <typename F>
-void parallel_ranges(size_t n, size_t min_per_thread, F&& fn) {
-  const size_t want = std::min<size_t>((size_t)host_threads(), std::max<size_t>(1, n / min_per_thread));
-  if (want <= 1) {
-    fn(0, n);
-    return;
-  }
-  const size_t step = (n + want - 1) / want;
-  const std::function<void(size_t)> part = [&](size_t t) {
-    const size_t lo = t * step, hi = std::min(n, lo + step);
-    if (lo < hi) fn(lo, hi);
-  };
-  host_pool().run(want, part);
-}
-
-void par_memcpy(void* dst, const void* src, size_t bytes) {
-  parallel_ranges(bytes, (size_t)512 << 10, [&](size_t lo, size_t hi) {
-    std::memcpy((uint8_t*)dst + lo, (const uint8_t*)src + lo, hi - lo);
-  });
 }
 
 // --------------------------------------------------------------------------
@@ -332,75 +231,6 @@ int current_ctx(DevCtx** out) {
   for (size_t i = 0; i < g_phys.size(); i++)
     if (g_phys[i] == dev) return get_ctx((int)i, out);
   return fail(GAES_EINVAL, "current device is not in GAES_DEVICE_MAP");
-}
-
-// --------------------------------------------------------------------------
-// Round keys.
-inline uint32_t le32(const uint8_t* p) {
-  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
-}
-
-// out byte r of column = XOR_j lut[r][j][b_j]  (_kernel.pyx:44-47 applied to a key column)
-uint32_t mix_word_lut(uint32_t w, const uint8_t* lut) {
-  uint32_t o = 0;
-  for (int r = 0; r < 4; r++) {
-    uint8_t acc = 0;
-    for (int j = 0; j < 4; j++) acc ^= lut[(r * 4 + j) * 256 + ((w >> (8 * j)) & 0xFF)];
-    o |= (uint32_t)acc << (8 * r);
-  }
-  return o;
-}
-
-uint32_t inv_mix_word_std(uint32_t w) {
-  uint32_t o = 0;
-  for (int r = 0; r < 4; r++) {
-    uint8_t acc = 0;
-    for (int j = 0; j < 4; j++) acc ^= gf_mul(mix_coef(true, r, j), (uint8_t)(w >> (8 * j)));
-    o |= (uint32_t)acc << (8 * r);
-  }
-  return o;
-}
-
-// fold: XOR the shared IV into the first (encrypt) / last (decrypt) key.
-RoundKeys make_enc_keys(const uint8_t* rk, const uint8_t* iv, bool fold) {
-  RoundKeys k;
-  for (int i = 0; i < 44; i++) k.w[i] = le32(rk + 4 * i);
-  for (int c = 0; c < 4; c++) {
-    k.iv[c] = iv ? le32(iv + 4 * c) : 0u;
-    if (fold) k.w[c] ^= k.iv[c];
-  }
-  return k;
-}
-
-RoundKeys make_dec_keys(const uint8_t* rk, const uint8_t* iv, bool fold, const uint8_t* inv_lut) {
-  RoundKeys k;
-  for (int i = 0; i < 44; i++) {
-    const uint32_t w = le32(rk + 4 * i);
-    if (i >= 4 && i < 40)
-      k.w[i] = inv_lut ? mix_word_lut(w, inv_lut) : inv_mix_word_std(w);
-    else
-      k.w[i] = w;
-  }
-  for (int c = 0; c < 4; c++) {
-    k.iv[c] = iv ? le32(iv + 4 * c) : 0u;
-    if (fold) k.w[c] ^= k.iv[c];
-  }
-  return k;
-}
-
-// Each lut[r][j] row must be GF(2)-linear for the equivalent inverse cipher.
-bool lut_is_linear(const uint8_t* lut) {
-  for (int t = 0; t < 16; t++) {
-    const uint8_t* row = lut + t * 256;
-    if (row[0] != 0) return false;
-    for (int x = 1; x < 256; x++) {
-      uint8_t acc = 0;
-      for (int b = 0; b < 8; b++)
-        if (x & (1 << b)) acc ^= row[1 << b];
-      if (row[x] != acc) return false;
-    }
-  }
-  return true;
 }
 
 // Compact T tables for caller-supplied (box, lut), cached per device.
