@@ -298,13 +298,6 @@ struct Job {
   uint8_t* out = nullptr;
   size_t n = 0, m = 16;
   RoundKeys rk;
-  // auto_iv: ivs may be a shared IV tiled into rows (IVSet.rows,
-  // aes_cbc.py:107-115).  Each chunk compares its rows with iv0 (row 0 of
-  // the whole grid) while staging; equal chunks skip the IV upload and use
-  // rk_folded (M = 16) or rk with rk.iv = iv0.
-  bool auto_iv = false;
-  const uint8_t* iv0 = nullptr;
-  RoundKeys rk_folded;
   const uint8_t* raw_rk = nullptr;  // generic path
   const uint8_t *box = nullptr, *lut = nullptr, *perm = nullptr;
   bool standard = true;  // use the device GF tables
@@ -360,38 +353,30 @@ int finish_slot(Slot& s) {
   return GAES_OK;
 }
 
-// One chunk's kernel.  iv_rows: the chunk's per-row IVs were uploaded to
-// s.d_iv (otherwise the IV is shared: folded into the keys or rk.iv).
-int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t rows, const uint32_t* compact, bool iv_rows) {
+int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t rows, const uint32_t* compact) {
   const uint64_t bpr = j.m / 16;
   const uint64_t nblk = rows * bpr;
-  Mode mode = j.mode;
-  const RoundKeys* rk = &j.rk;
-  if (j.auto_iv && !iv_rows && bpr == 1) {
-    mode = Mode::kFolded;
-    rk = &j.rk_folded;
-  }
-  switch (mode) {
+  switch (j.mode) {
     case Mode::kFolded:
       if (j.dec) {
-        GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, *rk, nullptr, 1,
+        GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,
                               c->sms, s.stream));
         note_kernel("k_blocks_dec_folded");
       } else if (j.standard || g_variant.load() < 2) {
-        GAES_CK(launch_enc_folded(c, s.d_in, s.d_out, nblk, compact, *rk, ilp_default(), s.stream));
+        GAES_CK(launch_enc_folded(c, s.d_in, s.d_out, nblk, compact, j.rk, ilp_default(), s.stream));
       } else {  // bitsliced kernel has the standard S-box built in; caller tables -> T-table
-        GAES_CK(launch_blocks(false, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, *rk, nullptr, 1,
+        GAES_CK(launch_blocks(false, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,
                               c->sms, s.stream));
         note_kernel("k_blocks_enc_folded");
       }
       break;
     case Mode::kChain:
-      GAES_CK(launch_blocks(j.dec, kIvChain, ilp_default(), s.d_in, s.d_out, nblk, compact, *rk,
-                            iv_rows ? s.d_iv : nullptr, bpr, c->sms, s.stream));
+      GAES_CK(launch_blocks(j.dec, kIvChain, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk,
+                            j.ivs ? s.d_iv : nullptr, bpr, c->sms, s.stream));
       note_kernel(j.dec ? "k_blocks_dec_chain" : "k_blocks_enc_chain");
       break;
     case Mode::kEncRows:
-      GAES_CK(launch_cbc_enc_rows(s.d_in, s.d_out, rows, bpr, compact, *rk, iv_rows ? s.d_iv : nullptr, c->sms,
+      GAES_CK(launch_cbc_enc_rows(s.d_in, s.d_out, rows, bpr, compact, j.rk, j.ivs ? s.d_iv : nullptr, c->sms,
                                   s.stream));
       note_kernel("k_cbc_enc_rows");
       break;
@@ -404,27 +389,6 @@ int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t rows, const uint32_t* 
     }
   }
   return GAES_OK;
-}
-
-// True if rows [0, n) of ivs all equal iv0 (parallel scan, early exit).
-bool rows_equal(const uint8_t* ivs, size_t n, const uint8_t* iv0) {
-  std::atomic<bool> same{true};
-  uint64_t a0, a1;
-  std::memcpy(&a0, iv0, 8);
-  std::memcpy(&a1, iv0 + 8, 8);
-  parallel_ranges(n, (size_t)1 << 16, [&](size_t lo, size_t hi) {
-    for (size_t i = lo; i < hi; i++) {
-      uint64_t b0, b1;
-      std::memcpy(&b0, ivs + 16 * i, 8);
-      std::memcpy(&b1, ivs + 16 * i + 8, 8);
-      if ((a0 ^ b0) | (a1 ^ b1)) {
-        same.store(false, std::memory_order_relaxed);
-        return;
-      }
-      if ((i & 4095) == 0 && !same.load(std::memory_order_relaxed)) return;
-    }
-  });
-  return same.load();
 }
 
 // Runs rows [0, j.n) of `j` on device context c (one shard).
@@ -517,8 +481,7 @@ int run_job(DevCtx* c, const Job& j) {
       src = s.h_in;
     }
     GAES_CK(cudaMemcpyAsync(s.d_in, src, bytes, cudaMemcpyHostToDevice, s.stream));
-    const bool iv_rows = need_iv && !(j.auto_iv && rows_equal(j.ivs + r0 * 16, rows, j.iv0));
-    if (iv_rows) {
+    if (need_iv) {
       const uint8_t* ivsrc = j.ivs + r0 * 16;
       if (!iv_pinned) {
         par_memcpy(s.h_iv, ivsrc, rows * 16);
@@ -526,7 +489,7 @@ int run_job(DevCtx* c, const Job& j) {
       }
       GAES_CK(cudaMemcpyAsync(s.d_iv, ivsrc, rows * 16, cudaMemcpyHostToDevice, s.stream));
     }
-    int rc = launch_chunk(c, j, s, rows, compact, iv_rows);
+    int rc = launch_chunk(c, j, s, rows, compact);
     if (rc) return rc;
     if (out_pinned) {
       GAES_CK(cudaMemcpyAsync(j.out + off, s.d_out, bytes, cudaMemcpyDeviceToHost, s.stream));
@@ -603,6 +566,28 @@ int run_sharded(const Job& j) {
   return GAES_OK;
 }
 
+// IVSet.rows tiles a shared IV into N x 16 (aes_cbc.py:107-115); detect it so
+// the IV folds into the key and the grid never crosses PCIe.
+bool rows_share_iv(const uint8_t* ivs, size_t n) {
+  std::atomic<bool> same{true};
+  parallel_ranges(n, (size_t)1 << 18, [&](size_t lo, size_t hi) {
+    uint64_t a0, a1;
+    std::memcpy(&a0, ivs, 8);
+    std::memcpy(&a1, ivs + 8, 8);
+    for (size_t i = std::max<size_t>(lo, 1); i < hi; i++) {
+      uint64_t b0, b1;
+      std::memcpy(&b0, ivs + 16 * i, 8);
+      std::memcpy(&b1, ivs + 16 * i + 8, 8);
+      if ((a0 ^ b0) | (a1 ^ b1)) {
+        same.store(false, std::memory_order_relaxed);
+        return;
+      }
+      if ((i & 4095) == 0 && !same.load(std::memory_order_relaxed)) return;
+    }
+  });
+  return same.load();
+}
+
 int check_grid(const void* data, const void* out, size_t n, size_t m) {
   if (n == 0) return GAES_OK;
   if (!data || !out) return fail(GAES_EINVAL, "null data/out pointer");
@@ -641,18 +626,17 @@ int cbc_host(bool dec, const uint8_t* data, const uint8_t* ivs, size_t n, size_t
     return run_sharded(j);
   }
   const size_t bpr = m / 16;
-  j.auto_iv = true;
-  j.ivs = ivs;
-  j.iv0 = ivs;
-  if (bpr == 1) {
+  const bool shared = rows_share_iv(ivs, n);
+  if (bpr == 1 && shared) {
+    j.mode = Mode::kFolded;
+    j.rk = dec ? make_dec_keys(rk, ivs, true, lut) : make_enc_keys(rk, ivs, true);
+  } else if (dec || bpr == 1) {
     j.mode = Mode::kChain;
+    j.ivs = shared ? nullptr : ivs;
     j.rk = dec ? make_dec_keys(rk, ivs, false, lut) : make_enc_keys(rk, ivs, false);
-    j.rk_folded = dec ? make_dec_keys(rk, ivs, true, lut) : make_enc_keys(rk, ivs, true);
-  } else if (dec) {
-    j.mode = Mode::kChain;
-    j.rk = make_dec_keys(rk, ivs, false, lut);
   } else {
     j.mode = Mode::kEncRows;
+    j.ivs = shared ? nullptr : ivs;
     j.rk = make_enc_keys(rk, ivs, false);
   }
   return run_sharded(j);
