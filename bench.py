@@ -374,7 +374,8 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    # ---- timed region: per-step CUDA events on the launching stream
+    # ---- timed region: CUDA events on the launching stream (per step when L2 is
+    # flushed between steps, else one pair around K back-to-back steps)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
