@@ -64,17 +64,23 @@ def test_full_size_single_key_configs(cfg):
     ph, chost = p.cpu().numpy(), c.cpu().numpy()
     assert ph.shape[0] == bench.WORKLOADS[cfg]["blocks"]
     assert _openssl_matches(inp["key"], np.frombuffer(inp["iv"], np.uint8), ph, chost)
+    if cfg == 4:  # deterministic encryption: #unique(C) == #unique(P)
+        up = torch.unique(p.view(torch.int64), dim=0).shape[0]
+        uc = torch.unique(c.view(torch.int64), dim=0).shape[0]
+        assert up == uc and up <= 10 ** 6
     back = device.BlockCipher(rk, inp["iv"]).decrypt(c, out=c)
     assert torch.equal(back, p)
     del p, c, back
     torch.cuda.empty_cache()
 
 
-def test_full_size_many_key_config5():
+def test_full_size_many_key_config5(oracle):
     dev = torch.device("cuda", 0)
     inp = bench.make_inputs(5, 0, 1, dev)
     p, keys, ivs, bpk = inp["p"], inp["keys"], inp["ivs"], inp["bpk"]
     rk_enc, rk_dec = device.expand_keys(torch.from_numpy(keys).to(dev))
+    # all 1024 GPU round-key schedules vs gen_keys (the oracle is pinned to it)
+    assert np.array_equal(rk_enc.cpu().numpy(), oracle.gen_keys_batch(keys))
     d_ivs = torch.from_numpy(ivs).to(dev)
     c = device.many_key_encrypt(p, rk_enc, d_ivs)
     ok = True
