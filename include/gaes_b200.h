@@ -127,6 +127,16 @@ GAES_API int gaes_cbc_encrypt_std(const uint8_t *data, const uint8_t *ivs, size_
 GAES_API int gaes_cbc_decrypt_std(const uint8_t *data, const uint8_t *ivs, size_t n, size_t m,
                                   const uint8_t round_keys[176], uint8_t *out);
 
+/* Many-key batch with host buffers (config 5 end to end): key i owns rows
+ * [i*blocks_per_key, (i+1)*blocks_per_key) of data/out (u8[k*bpk][16]);
+ * keys u8[k][16] and per-key shared IVs u8[k][16] (NULL = zero IV) on the
+ * host.  The key schedule runs on each GPU used (gaes_expand_keys_dev);
+ * rows are sharded across gaes_get_num_gpus() devices. */
+GAES_API int gaes_many_key_encrypt(const uint8_t *data, size_t blocks_per_key, size_t k, const uint8_t *keys,
+                                   const uint8_t *ivs, uint8_t *out);
+GAES_API int gaes_many_key_decrypt(const uint8_t *data, size_t blocks_per_key, size_t k, const uint8_t *keys,
+                                   const uint8_t *ivs, uint8_t *out);
+
 /* ---- device-resident entry points (stream-ordered, current device) ----
  * Standard tables from the device GF layer.  `iv` is a 16-byte HOST
  * array (shared IV, folded into the round keys) or NULL for a zero IV. */

@@ -37,6 +37,8 @@ SIGNATURES = {
     "gaes_cbc_decrypt": (_i, [_vp, _vp, _sz, _sz, _vp, _vp, _vp, _vp, _vp]),
     "gaes_cbc_encrypt_std": (_i, [_vp, _vp, _sz, _sz, _vp, _vp]),
     "gaes_cbc_decrypt_std": (_i, [_vp, _vp, _sz, _sz, _vp, _vp]),
+    "gaes_many_key_encrypt": (_i, [_vp, _sz, _sz, _vp, _vp, _vp]),
+    "gaes_many_key_decrypt": (_i, [_vp, _sz, _sz, _vp, _vp, _vp]),
     "gaes_encrypt_shared_iv": (_i, [_vp, _sz, _sz, _vp, _vp, _vp]),
     "gaes_decrypt_shared_iv": (_i, [_vp, _sz, _sz, _vp, _vp, _vp]),
     "gaes_encrypt_blocks_dev": (_i, [_vp, _vp, _sz, _vp, _vp, _vp]),

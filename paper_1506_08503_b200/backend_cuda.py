@@ -177,3 +177,34 @@ def standard_tables(decrypt: bool = False):
     perm = np.empty(16, np.uint8)
     _lib.check(_lib.lib().gaes_std_tables(int(bool(decrypt)), _ptr(box), _ptr(lut), _ptr(perm)))
     return box, lut, perm
+
+
+def _many_key(dec: bool, data, keys, ivs=None, out=None) -> np.ndarray:
+    data = _buf(data, "data", 2)
+    keys = _buf(np.ascontiguousarray(keys, np.uint8), "keys", 2)
+    n, m = data.shape
+    k = keys.shape[0]
+    if m != 16 or keys.shape[1] != 16 or k == 0 or n % k:
+        raise ValueError("many-key batches are N x 16 rows, keys K x 16 with N a multiple of K")
+    if ivs is not None:
+        ivs = _buf(np.ascontiguousarray(ivs, np.uint8), "ivs", 2)
+        if ivs.shape != (k, 16):
+            raise ValueError("ivs must be K x 16")
+    if out is None:
+        out = np.empty_like(data)
+    out = _buf(out, "out", 2, writable=True)
+    if out.shape != data.shape:
+        raise ValueError("out must match data")
+    fn = _lib.lib().gaes_many_key_decrypt if dec else _lib.lib().gaes_many_key_encrypt
+    _lib.check(fn(_ptr(data), n // k, k, _ptr(keys), _ptr(ivs) if ivs is not None else None, _ptr(out)))
+    return out
+
+
+def many_key_encrypt(data, keys, ivs=None, out=None) -> np.ndarray:
+    """Host-buffer many-key batch (config 5): key i encrypts rows [i*N/K, (i+1)*N/K)
+    with its own shared IV ivs[i]; key schedule on the GPU."""
+    return _many_key(False, data, keys, ivs, out)
+
+
+def many_key_decrypt(data, keys, ivs=None, out=None) -> np.ndarray:
+    return _many_key(True, data, keys, ivs, out)

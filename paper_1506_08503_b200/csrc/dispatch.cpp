@@ -96,11 +96,13 @@ struct DevCtx {
   std::unordered_map<std::string, uint32_t*> cache;  // (box || lut) -> compact tables
   uint8_t* d_scratch = nullptr;  // box(256) lut(4096) perm(16) rk(176)
   uint8_t* d_tmp = nullptr;      // GF-build outputs + error flag
+  uint8_t* d_mk = nullptr;       // many-key: keys | rk (K x 176) | ivs
+  size_t mk_cap = 0;
   Slot slots[kSlots];
   // Only runs when initialisation fails (live contexts are never destroyed:
   // freeing after the CUDA runtime has shut down at exit is not allowed).
   ~DevCtx() {
-    for (void* p : {(void*)d_std_enc, (void*)d_std_dec, (void*)d_scratch, (void*)d_tmp})
+    for (void* p : {(void*)d_std_enc, (void*)d_std_dec, (void*)d_scratch, (void*)d_tmp, (void*)d_mk})
       if (p) cudaFree(p);
     for (auto& s : slots) {
       if (s.stream) cudaStreamDestroy(s.stream);
@@ -288,7 +290,7 @@ cudaError_t launch_enc_folded(DevCtx* c, const void* in, void* out, uint64_t n, 
 
 // --------------------------------------------------------------------------
 // Host-buffer pipeline.
-enum class Mode { kFolded, kChain, kEncRows, kGeneric };
+enum class Mode { kFolded, kChain, kEncRows, kGeneric, kManyKey };
 
 struct Job {
   bool dec = false;
@@ -301,6 +303,11 @@ struct Job {
   const uint8_t* raw_rk = nullptr;  // generic path
   const uint8_t *box = nullptr, *lut = nullptr, *perm = nullptr;
   bool standard = true;  // use the device GF tables
+  // kManyKey: key i owns global blocks [i*bpk, (i+1)*bpk); this job's rows
+  // start at global block `first`; keys / per-key IVs are host arrays.
+  size_t bpk = 0, first = 0, n_keys = 0;
+  const uint8_t* mk_keys = nullptr;
+  const uint8_t* mk_ivs = nullptr;
 };
 
 bool is_pinned(const void* p) {
@@ -353,7 +360,7 @@ int finish_slot(Slot& s) {
   return GAES_OK;
 }
 
-int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t rows, const uint32_t* compact) {
+int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t r0, size_t rows, const uint32_t* compact) {
   const uint64_t bpr = j.m / 16;
   const uint64_t nblk = rows * bpr;
   switch (j.mode) {
@@ -380,6 +387,14 @@ int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t rows, const uint32_t* 
                                   s.stream));
       note_kernel("k_cbc_enc_rows");
       break;
+    case Mode::kManyKey: {
+      const size_t kb = j.n_keys * 16, rkb = j.n_keys * 176;
+      GAES_CK(launch_many_key(j.dec, s.d_in, s.d_out, nblk, j.first + r0, j.bpk, compact,
+                              c->d_mk + kb + (j.dec ? rkb : 0), j.mk_ivs ? c->d_mk + kb + 2 * rkb : nullptr, c->sms,
+                              s.stream));
+      note_kernel(j.dec ? "k_many_key_dec" : "k_many_key_enc");
+      break;
+    }
     case Mode::kGeneric: {
       uint8_t* sc = c->d_scratch;
       GAES_CK(launch_generic(j.dec, s.d_in, s.d_iv, rows, j.m, sc + 256 + 4096 + 16, sc, sc + 256, sc + 256 + 4096,
@@ -430,6 +445,29 @@ int run_job(DevCtx* c, const Job& j) {
     GAES_CK(cudaMemcpy(sc + 256, j.lut, 4096, cudaMemcpyHostToDevice));
     GAES_CK(cudaMemcpy(sc + 256 + 4096, j.perm, 16, cudaMemcpyHostToDevice));
     GAES_CK(cudaMemcpy(sc + 256 + 4096 + 16, j.raw_rk, 176, cudaMemcpyHostToDevice));
+  }
+
+  if (j.mode == Mode::kManyKey) {
+    // keys (and per-key IVs) to the device, batched key schedule there
+    // layout: keys (K x 16) | rk_enc (K x 176) | rk_dec (K x 176) | ivs (K x 16)
+    const size_t need = j.n_keys * (16 + 176 + 176 + 16);
+    if (c->mk_cap < need) {
+      if (c->d_mk) cudaFree(c->d_mk);
+      c->d_mk = nullptr;
+      c->mk_cap = 0;
+      GAES_CK(cudaMalloc(&c->d_mk, need));
+      c->mk_cap = need;
+    }
+    const size_t kb = j.n_keys * 16;
+    cudaStream_t s0 = c->slots[0].stream;
+    GAES_CK(cudaMemcpyAsync(c->d_mk, j.mk_keys, kb, cudaMemcpyHostToDevice, s0));
+    if (j.mk_ivs)
+      GAES_CK(cudaMemcpyAsync(c->d_mk + kb + 2 * j.n_keys * 176, j.mk_ivs, kb, cudaMemcpyHostToDevice, s0));
+    // encrypt and equivalent-inverse-cipher (decrypt) schedules
+    GAES_CK(launch_expand_keys(c->d_mk, j.n_keys, c->d_std_enc, c->d_mk + kb,
+                               j.dec ? c->d_mk + kb + j.n_keys * 176 : nullptr, s0));
+    note_kernel("k_expand_keys");
+    GAES_CK(cudaStreamSynchronize(s0));
   }
 
   const bool in_pinned = is_pinned(j.data);
@@ -489,7 +527,7 @@ int run_job(DevCtx* c, const Job& j) {
       }
       GAES_CK(cudaMemcpyAsync(s.d_iv, ivsrc, rows * 16, cudaMemcpyHostToDevice, s.stream));
     }
-    int rc = launch_chunk(c, j, s, rows, compact);
+    int rc = launch_chunk(c, j, s, r0, rows, compact);
     if (rc) return rc;
     if (out_pinned) {
       GAES_CK(cudaMemcpyAsync(j.out + off, s.d_out, bytes, cudaMemcpyDeviceToHost, s.stream));
@@ -548,6 +586,7 @@ int run_sharded(const Job& j) {
     s.data = j.data + chunks[i].first * j.m;
     s.out = j.out + chunks[i].first * j.m;
     if (j.ivs) s.ivs = j.ivs + chunks[i].first * 16;
+    s.first = j.first + chunks[i].first;
     s.n = chunks[i].second - chunks[i].first;
     return s;
   };
@@ -810,6 +849,35 @@ GAES_API int gaes_cbc_decrypt_std(const uint8_t* data, const uint8_t* ivs, size_
   return cbc_host(true, data, ivs, n, m, round_keys, c->std_inv, c->std_mix_inv, kInvShiftRowsSrc, out);
 }
 
+static int many_key_host(bool dec, const uint8_t* data, size_t bpk, size_t k, const uint8_t* keys,
+                         const uint8_t* ivs, uint8_t* out) {
+  if (bpk == 0 || k == 0) return GAES_OK;
+  if (!data || !out || !keys) return fail(GAES_EINVAL, "null pointer");
+  Job j;
+  j.dec = dec;
+  j.mode = Mode::kManyKey;
+  j.data = data;
+  j.out = out;
+  j.n = bpk * k;
+  j.m = 16;
+  j.bpk = bpk;
+  j.n_keys = k;
+  j.mk_keys = keys;
+  j.mk_ivs = ivs;
+  j.standard = true;
+  return run_sharded(j);
+}
+
+GAES_API int gaes_many_key_encrypt(const uint8_t* data, size_t blocks_per_key, size_t k, const uint8_t* keys,
+                                   const uint8_t* ivs, uint8_t* out) {
+  return many_key_host(false, data, blocks_per_key, k, keys, ivs, out);
+}
+
+GAES_API int gaes_many_key_decrypt(const uint8_t* data, size_t blocks_per_key, size_t k, const uint8_t* keys,
+                                   const uint8_t* ivs, uint8_t* out) {
+  return many_key_host(true, data, blocks_per_key, k, keys, ivs, out);
+}
+
 GAES_API int gaes_encrypt_shared_iv(const uint8_t* data, size_t n, size_t m, const uint8_t iv[16],
                                     const uint8_t round_keys[176], uint8_t* out) {
   return shared_iv_host(false, data, n, m, iv, round_keys, out);
@@ -904,7 +972,7 @@ GAES_API int gaes_many_key_encrypt_dev(const void* in, void* out, size_t blocks_
   DevCtx* c = nullptr;
   int rc = current_ctx(&c);
   if (rc) return rc;
-  GAES_CK(launch_many_key(false, in, out, blocks_per_key, k, c->d_std_enc, rk_enc, ivs_dev, c->sms,
+  GAES_CK(launch_many_key(false, in, out, blocks_per_key * k, 0, blocks_per_key, c->d_std_enc, rk_enc, ivs_dev, c->sms,
                           (cudaStream_t)stream));
   note_kernel("k_many_key_enc");
   return GAES_OK;
@@ -917,7 +985,7 @@ GAES_API int gaes_many_key_decrypt_dev(const void* in, void* out, size_t blocks_
   DevCtx* c = nullptr;
   int rc = current_ctx(&c);
   if (rc) return rc;
-  GAES_CK(launch_many_key(true, in, out, blocks_per_key, k, c->d_std_dec, rk_dec, ivs_dev, c->sms,
+  GAES_CK(launch_many_key(true, in, out, blocks_per_key * k, 0, blocks_per_key, c->d_std_dec, rk_dec, ivs_dev, c->sms,
                           (cudaStream_t)stream));
   note_kernel("k_many_key_dec");
   return GAES_OK;

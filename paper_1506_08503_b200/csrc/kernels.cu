@@ -357,17 +357,19 @@ __global__ void k_expand_keys(const uint8_t* __restrict__ keys, uint64_t k, cons
 }
 
 // ---------------------------------------------------------------------------
-// Many-key batch: key i owns blocks [i*bpk, (i+1)*bpk).  Round keys live in
-// registers and are reloaded only when a thread's walk through its CTA's
-// contiguous range crosses into the next key's blocks.
+// Many-key batch: key i owns global blocks [i*bpk, (i+1)*bpk).  A launch
+// covers n_blocks blocks starting at global block `first` (so host pipelines
+// may cut chunks anywhere).  Round keys live in registers and are reloaded
+// only when a thread's walk through its CTA's contiguous range crosses into
+// the next key's blocks.
 template <bool DEC>
 __global__ void __launch_bounds__(kManyKeyThreads, 1)
-    k_many_key(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t bpk, uint64_t n_keys,
-               const uint32_t* __restrict__ compact, const uint4* __restrict__ rks, const uint4* __restrict__ ivs) {
+    k_many_key(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks, uint64_t first,
+               uint64_t bpk, const uint32_t* __restrict__ compact, const uint4* __restrict__ rks,
+               const uint4* __restrict__ ivs) {
   extern __shared__ __align__(1024) char smem[];
   pdl_prologue(smem, compact);
   const uint32_t lb = (threadIdx.x & 31) * 4;
-  const uint64_t n_blocks = bpk * n_keys;
   // Each CTA owns one contiguous range and its threads stride by blockDim
   // inside it, so a thread crosses into the next key only at real key
   // boundaries (grid-wide striding would reload keys on every block when
@@ -377,8 +379,8 @@ __global__ void __launch_bounds__(kManyKeyThreads, 1)
   const uint64_t hi = min(n_blocks, lo + per_cta);
   uint64_t b = lo + threadIdx.x;
   if (b >= hi) return;
-  uint64_t key = b / bpk;
-  uint64_t key_end = (key + 1) * bpk;
+  uint64_t key = (first + b) / bpk;
+  uint64_t key_end = (key + 1) * bpk - first;  // in launch-local block units
   RoundKeys rk;
   auto load_key = [&](uint64_t kid) {
 #pragma unroll
@@ -396,8 +398,8 @@ __global__ void __launch_bounds__(kManyKeyThreads, 1)
     uint4 nxt = cur;
     if (nb < hi) nxt = ld_stream(in + nb);
     if (b >= key_end) {
-      key = b / bpk;
-      key_end = (key + 1) * bpk;
+      key = (first + b) / bpk;
+      key_end = (key + 1) * bpk - first;
       load_key(key);
     }
     uint32_t s0 = cur.x, s1 = cur.y, s2 = cur.z, s3 = cur.w;
@@ -601,14 +603,15 @@ cudaError_t launch_expand_keys(const uint8_t* keys, uint64_t k, const uint32_t* 
   return cudaGetLastError();
 }
 
-cudaError_t launch_many_key(bool dec, const void* in, void* out, uint64_t bpk, uint64_t n_keys,
+cudaError_t launch_many_key(bool dec, const void* in, void* out, uint64_t n_blocks, uint64_t first, uint64_t bpk,
                             const uint32_t* compact, const void* rks, const void* ivs, int sms, cudaStream_t s) {
-  if (bpk == 0 || n_keys == 0) return cudaSuccess;
+  if (bpk == 0 || n_blocks == 0) return cudaSuccess;
   cudaError_t e = dec ? set_smem(k_many_key<true>) : set_smem(k_many_key<false>);
   if (e != cudaSuccess) return e;
-  const int grid = grid_for(bpk * n_keys, 1, sms, kManyKeyThreads);
+  const int grid = grid_for(n_blocks, 1, sms, kManyKeyThreads);
   return launch_pdl(dec ? k_many_key<true> : k_many_key<false>, grid, kManyKeyThreads, kSmemBytes, s,
-                    (const uint4*)in, (uint4*)out, bpk, n_keys, compact, (const uint4*)rks, (const uint4*)ivs);
+                    (const uint4*)in, (uint4*)out, n_blocks, first, bpk, compact, (const uint4*)rks,
+                    (const uint4*)ivs);
 }
 
 }  // namespace gaes

@@ -553,6 +553,15 @@ for n, m in [(1, 16), (3, 16), (100001, 16), (5003, 48)]:
         assert np.array_equal(back, data), (n, m, g)
         ct = backend_cuda.encrypt_shared_iv(data, iv, rk)
         assert np.array_equal(backend_cuda.decrypt_shared_iv(ct, iv, rk), data)
+keys = rng.integers(0, 256, (7, 16), dtype=np.uint8)
+kivs = rng.integers(0, 256, (7, 16), dtype=np.uint8)
+p = rng.integers(0, 256, (7 * 10001, 16), dtype=np.uint8)
+outs = []
+for g in (1, 2):
+    _lib.set_num_gpus(g)
+    outs.append(backend_cuda.many_key_encrypt(p, keys, kivs))
+    assert np.array_equal(backend_cuda.many_key_decrypt(outs[-1], keys, kivs), p)
+assert np.array_equal(outs[0], outs[1])
 print("ok")
 '''
     import os
@@ -654,3 +663,20 @@ def test_concurrent_device_api_on_streams(oracle):
         assert torch.equal(outs[i], device.encrypt_blocks(xs[i], rk, iv))
     ivrows = np.tile(np.frombuffer(iv, np.uint8), (1000, 1))
     assert np.array_equal(outs[0][:1000].cpu().numpy(), oracle.encrypt(key, ivrows, xs[0][:1000].cpu().numpy()))
+
+
+@pytest.mark.parametrize("k,bpk", [(1, 1), (3, 1000), (64, 4099), (5, 300000)])
+def test_host_many_key_matches_oracle(oracle, k, bpk):
+    """Host-buffer many-key entry (config 5 end to end): GPU key schedule + pipeline."""
+    rng = np.random.default_rng(k * 7 + bpk)
+    keys = rng.integers(0, 256, (k, 16), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (k, 16), dtype=np.uint8)
+    p = rng.integers(0, 256, (k * bpk, 16), dtype=np.uint8)
+    c = backend_cuda.many_key_encrypt(p, keys, ivs)
+    for i in sorted({0, k // 2, k - 1}):
+        rows = slice(i * bpk, (i + 1) * bpk)
+        ivrows = np.tile(ivs[i], (bpk, 1))
+        assert np.array_equal(c[rows], oracle.encrypt(keys[i].tobytes(), ivrows, p[rows], threads=4)), i
+    assert np.array_equal(backend_cuda.many_key_decrypt(c, keys, ivs), p)
+    c0 = backend_cuda.many_key_encrypt(p, keys)  # zero IVs
+    assert np.array_equal(c0[:bpk], oracle.encrypt(keys[0].tobytes(), np.zeros((bpk, 16), np.uint8), p[:bpk]))
