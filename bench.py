@@ -339,6 +339,9 @@ def main():
     launched = "RANK" in os.environ and "MASTER_ADDR" in os.environ  # torchrun, any world size
     if launched:
         dist.init_process_group("nccl", device_id=dev)
+    # host side of this rank (pinned staging, copy threads) on the GPU's NUMA node
+    from paper_1506_08503_b200.shard import bind_to_gpu_numa_node
+    numa_cpus = bind_to_gpu_numa_node(local) if world > 1 else None
     if args.variant:
         _lib.check(_lib.lib().gaes_set_variant(args.variant))
     # one process per GPU: host-buffer calls stay on this rank's device
@@ -644,7 +647,9 @@ def main():
             "config": {"workload": w["name"], "blocks_per_gpu": n, "total_blocks": total_blocks,
                        "l2": "L2 flushed between steps" if flush is not None else
                              "inputs larger than L2 (no flush)",
-                       "parallelism": f"dp{world} (contiguous block shards, no collective)", **inp["meta"]},
+                       "parallelism": f"dp{world} (contiguous block shards, no collective)",
+                       "host_cpus": (f"{len(numa_cpus)} CPUs local to the GPU" if numa_cpus else "all"),
+                       **inp["meta"]},
             "gpu_launches": launches, "roofline": roofline, "e2e": e2e, "e2e_dropin": dropin, "cpu_baseline": cpu,
             "clocks": clocks,
             "decrypt_gbs_per_gpu": round(dec_gbs, 2), "verified": verified, "verification": check,

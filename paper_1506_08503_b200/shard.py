@@ -87,3 +87,30 @@ def sum_over_ranks(value: int, device=None) -> int:
     t = torch.tensor([int(value)], dtype=torch.int64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return int(t.item())
+
+
+def bind_to_gpu_numa_node(device_index: int) -> list | None:
+    """Pin this process to the CPUs local to the GPU's PCIe root (one process
+    per GPU): pinned staging buffers and host copies then stay on the GPU's
+    NUMA node.  Best effort; returns the CPU list used or None."""
+    try:
+        import torch
+        props = torch.cuda.get_device_properties(device_index)
+        bdf = f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bdf}/local_cpulist") as f:
+            text = f.read().strip()
+        cpus = []
+        for part in text.split(","):
+            if "-" in part:
+                lo, hi = part.split("-")
+                cpus.extend(range(int(lo), int(hi) + 1))
+            elif part:
+                cpus.append(int(part))
+        allowed = os.sched_getaffinity(0)
+        cpus = [c for c in cpus if c in allowed]
+        if not cpus or len(cpus) == len(allowed):
+            return None
+        os.sched_setaffinity(0, cpus)
+        return cpus
+    except (OSError, ValueError, AttributeError, RuntimeError):
+        return None

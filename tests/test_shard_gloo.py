@@ -97,3 +97,11 @@ def test_plan_matches_reference_plan(oracle):
     for n in (0, 3, 100, 12345):
         for w in (1, 2, 3, 8):
             assert list(plan(n, w).chunks) == [tuple(c) for c in oracle.plan(n, w)]
+
+
+def test_numa_binding_is_best_effort():
+    from paper_1506_08503_b200.shard import bind_to_gpu_numa_node
+    # no GPU here: must not raise, must not change the affinity
+    before = os.sched_getaffinity(0)
+    assert bind_to_gpu_numa_node(0) is None
+    assert os.sched_getaffinity(0) == before
