@@ -58,6 +58,24 @@ def _p(a) -> int | None:
     return a.data_ptr()
 
 
+class _on_device:
+    """torch.cuda.device(d) only when d is not already current (the context
+    manager costs a few microseconds per call)."""
+
+    __slots__ = ("_ctx",)
+
+    def __init__(self, dev: torch.device):
+        self._ctx = None if dev.index == torch.cuda.current_device() else torch.cuda.device(dev)
+
+    def __enter__(self):
+        if self._ctx is not None:
+            self._ctx.__enter__()
+
+    def __exit__(self, *exc):
+        if self._ctx is not None:
+            self._ctx.__exit__(*exc)
+
+
 def _check_grid(x: torch.Tensor, out: torch.Tensor | None):
     x = _u8_cuda(x, "input", 2)
     if x.shape[1] == 0 or x.shape[1] % 16:
@@ -95,7 +113,7 @@ class BlockCipher:
         elif out.shape != x.shape or out.device != x.device or out.dtype != torch.uint8 or not out.is_contiguous():
             raise ValueError("out must match the input")
         if x.device.index != torch.cuda.current_device():
-            with torch.cuda.device(x.device):
+            with _on_device(x.device):
                 _lib.check(fn(x.data_ptr(), out.data_ptr(), x.shape[0], self._rk_p, self._iv_p, _stream()))
         else:
             _lib.check(fn(x.data_ptr(), out.data_ptr(), x.shape[0], self._rk_p, self._iv_p, _stream()))
@@ -115,7 +133,7 @@ def encrypt_blocks(x: torch.Tensor, round_keys, iv=None, out: torch.Tensor | Non
         raise ValueError("encrypt_blocks takes N x 16 rows; use cbc_encrypt for wider rows")
     rk = _host_bytes(round_keys, 176, "round_keys")
     ivb = _host_bytes(iv, 16, "iv")
-    with torch.cuda.device(x.device):
+    with _on_device(x.device):
         _lib.check(_lib.lib().gaes_encrypt_blocks_dev(_p(x), _p(out), x.shape[0], _p(rk), _p(ivb), _stream()))
     return out
 
@@ -126,7 +144,7 @@ def decrypt_blocks(x: torch.Tensor, round_keys, iv=None, out: torch.Tensor | Non
         raise ValueError("decrypt_blocks takes N x 16 rows; use cbc_decrypt for wider rows")
     rk = _host_bytes(round_keys, 176, "round_keys")
     ivb = _host_bytes(iv, 16, "iv")
-    with torch.cuda.device(x.device):
+    with _on_device(x.device):
         _lib.check(_lib.lib().gaes_decrypt_blocks_dev(_p(x), _p(out), x.shape[0], _p(rk), _p(ivb), _stream()))
     return out
 
@@ -148,7 +166,7 @@ def cbc_encrypt(x: torch.Tensor, round_keys, ivs=None, out: torch.Tensor | None 
     x, out = _check_grid(x, out)
     rk = _host_bytes(round_keys, 176, "round_keys")
     d_ivs, ivb = _ivs(ivs, x.shape[0], x.device)
-    with torch.cuda.device(x.device):
+    with _on_device(x.device):
         _lib.check(_lib.lib().gaes_cbc_encrypt_dev(_p(x), _p(out), x.shape[0], x.shape[1], _p(d_ivs), _p(ivb),
                                                    _p(rk), _stream()))
     return out
@@ -158,7 +176,7 @@ def cbc_decrypt(x: torch.Tensor, round_keys, ivs=None, out: torch.Tensor | None 
     x, out = _check_grid(x, out)
     rk = _host_bytes(round_keys, 176, "round_keys")
     d_ivs, ivb = _ivs(ivs, x.shape[0], x.device)
-    with torch.cuda.device(x.device):
+    with _on_device(x.device):
         _lib.check(_lib.lib().gaes_cbc_decrypt_dev(_p(x), _p(out), x.shape[0], x.shape[1], _p(d_ivs), _p(ivb),
                                                    _p(rk), _stream()))
     return out
@@ -172,7 +190,7 @@ def expand_keys(keys: torch.Tensor, with_decrypt: bool = True):
     k = keys.shape[0]
     rk_enc = torch.empty((k, 11, 16), dtype=torch.uint8, device=keys.device)
     rk_dec = torch.empty_like(rk_enc) if with_decrypt else None
-    with torch.cuda.device(keys.device):
+    with _on_device(keys.device):
         _lib.check(_lib.lib().gaes_expand_keys_dev(_p(keys), k, _p(rk_enc), _p(rk_dec), _stream()))
     return rk_enc, rk_dec
 
@@ -199,7 +217,7 @@ def _many_key(enc: bool, x, rks, ivs, out):
             raise ValueError("ivs must be K x 16")
     bpk = x.shape[0] // k
     fn = _lib.lib().gaes_many_key_encrypt_dev if enc else _lib.lib().gaes_many_key_decrypt_dev
-    with torch.cuda.device(x.device):
+    with _on_device(x.device):
         _lib.check(fn(_p(x), _p(out), bpk, k, _p(rks), _p(ivs), _stream()))
     return out
 

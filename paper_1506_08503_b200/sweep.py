@@ -79,7 +79,7 @@ def _time(fn, reps: int, warmup: int, sync=None):
 
 def measure_point(kind: str, n: int, length: int, seed: int = 2016, reps: int = 5, warmup: int = 1,
                   device_resident: bool = False):
-    from .device import encrypt_blocks, expand_key
+    from .device import expand_key
     rng = np.random.default_rng(seed)
     key, iv = rng.bytes(16), rng.bytes(16)
     width = 16 * ((length + 15) // 16)
@@ -93,9 +93,11 @@ def measure_point(kind: str, n: int, length: int, seed: int = 2016, reps: int = 
             x = torch.from_numpy(data).cuda()
             fn = lambda: dev_cbc(x, rk, iv)  # noqa: E731
         else:
+            from .device import BlockCipher
             x = torch.from_numpy(data).cuda()
             out = torch.empty_like(x)
-            fn = lambda: encrypt_blocks(x, rk, iv, out=out)  # noqa: E731
+            bc = BlockCipher(rk, iv)
+            fn = lambda: bc.encrypt(x, out=out)  # noqa: E731
         sec = _time(fn, reps, warmup, sync=torch.cuda.synchronize)
         impl = "cuda-device"
     else:
