@@ -30,6 +30,11 @@ from . import _lib, backend_cuda
 
 CSV_HEADER = ("kind,implementation,n_messages,message_len_bytes,workers,"
               "total_bytes,median_seconds,rate_bytes_per_second")
+# --extended appends (metrics): plaintext GB/s, fraction of the
+# measured HBM copy bandwidth (32 B moved per block), fraction of the
+# shared-memory lookup roofline (160 lookups per block at the sampled SM
+# clock) and that clock.
+EXTENDED_HEADER = CSV_HEADER + ",gbs,hbm_frac,lds_frac,sm_mhz"
 MIN_REGION_SECONDS = 0.010
 
 
@@ -77,6 +82,30 @@ def _time(fn, reps: int, warmup: int, sync=None):
     return median(ts)
 
 
+def _sm_mhz() -> float | None:
+    try:
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(
+            "{:08x}:{:02x}:{:02x}.0".format(*[getattr(torch.cuda.get_device_properties(0), k)
+                                               for k in ("pci_domain_id", "pci_bus_id", "pci_device_id")]))
+        return float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+    except Exception:  # pragma: no cover - informational
+        return None
+
+
+def _hbm_peak() -> float:
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6650.0
+
+
 def measure_point(kind: str, n: int, length: int, seed: int = 2016, reps: int = 5, warmup: int = 1,
                   device_resident: bool = False):
     from .device import expand_key
@@ -119,6 +148,7 @@ def main(argv=None) -> int:
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--seed", type=int, default=2016)
     ap.add_argument("--device-resident", action="store_true")
+    ap.add_argument("--extended", action="store_true", help="append gbs,hbm_frac,lds_frac,sm_mhz columns")
     ap.add_argument("--out", default="-")
     a = ap.parse_args(argv)
     _gate()
@@ -129,7 +159,17 @@ def main(argv=None) -> int:
     else:
         for ln in (int(v) for v in a.lengths.split(",")):
             rows.append(measure_point("length", a.n_messages, ln, a.seed, a.reps, device_resident=a.device_resident))
-    lines = [CSV_HEADER] + [f"{k},{i},{n},{ln},{w},{t},{s:.9f},{r:.3f}" for k, i, n, ln, w, t, s, r in rows]
+    lines = [EXTENDED_HEADER if a.extended else CSV_HEADER]
+    mhz = _sm_mhz() if a.extended else None
+    hbm = _hbm_peak()
+    for k, i, n, ln, w, t, sec, r in rows:
+        line = f"{k},{i},{n},{ln},{w},{t},{sec:.9f},{r:.3f}"
+        if a.extended:
+            blocks = n * ((ln + 15) // 16)
+            bps = blocks / sec
+            lds = f"{bps * 160 / (148 * 32 * mhz * 1e6):.4f}" if mhz else ""
+            line += f",{r / 1e9:.3f},{bps * 32 / 1e9 / hbm:.4f},{lds},{mhz or ''}"
+        lines.append(line)
     text = "\n".join(lines) + "\n"
     if a.out == "-":
         sys.stdout.write(text)

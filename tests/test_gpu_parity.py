@@ -433,6 +433,10 @@ def test_sweep_csv_schema(tmp_path):
     assert sweep.main(["--kind", "length", "--lengths", "16,100", "--reps", "3", "--device-resident",
                        "--out", str(out)]) == 0
     assert out.read_text().splitlines()[2].startswith("length,cuda-device,128,100,")
+    assert sweep.main(["--kind", "count", "--counts", "100000", "--reps", "3", "--device-resident", "--extended",
+                       "--out", str(out)]) == 0
+    head, row = out.read_text().splitlines()
+    assert head.endswith(",gbs,hbm_frac,lds_frac,sm_mhz") and len(row.split(",")) == 12
 
 
 def test_std_entry_points_match_oracle(oracle):
