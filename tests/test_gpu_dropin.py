@@ -134,3 +134,36 @@ def test_reference_test_suite_passes_on_cuda_backend():
     assert r.returncode == 0, tail
     assert " passed" in tail and "failed" not in tail, tail
 
+
+
+def test_integration_md_binding_works(gaes, tmp_path):
+    """The ctypes stub INTEGRATION.md tells a maintainer to add is a working backend."""
+    import importlib.util
+    import re
+    text = open(os.path.join(REPO, "INTEGRATION.md")).read()
+    stub = re.search(r"```python\n(# gaes/_kernel_cuda.py.*?)```", text, re.S).group(1)
+    lib_path = os.path.join(REPO, "paper_1506_08503_b200", "libgaes_b200.so")
+    stub = stub.replace('ctypes.CDLL("libgaes_b200.so")', f'ctypes.CDLL({lib_path!r})')
+    path = tmp_path / "_kernel_cuda.py"
+    path.write_text(stub)
+    spec = importlib.util.spec_from_file_location("_kernel_cuda_doc", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.NAME == "cuda"
+    prev = gaes.backend.name()
+    gaes.backend._BACKENDS["cuda_doc"] = mod
+    try:
+        rng = np.random.default_rng(99)
+        key = rng.bytes(16)
+        data = rng.integers(0, 256, (300, 32), dtype=np.uint8)
+        batch = gaes.MessageBatch(data=data, original_lens=(32,) * 300)
+        ivs = gaes.IVSet.shared(rng.bytes(16))
+        gaes.backend.select("compiled")
+        want = gaes.encrypt_batch(key, ivs, batch)
+        gaes.backend._active = mod  # the registry entry's module (its NAME is "cuda")
+        got = gaes.encrypt_batch(key, ivs, batch)
+        assert np.array_equal(got, want)
+        assert np.array_equal(gaes.decrypt_batch(key, ivs, got), data)
+    finally:
+        del gaes.backend._BACKENDS["cuda_doc"]
+        gaes.backend.select(prev)
