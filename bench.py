@@ -287,6 +287,39 @@ def cpu_baseline(key, iv, budget_s: float):
                       f"{threads} threads over parallel.plan chunks"}
 
 
+def openssl_rate(key: bytes, iv: bytes, budget_s: float = 3.0):
+    """OpenSSL AES-128-ECB of P ^ IV (AES-NI) on all host cores: the paper's
+    own comparand, reported beside cpu_baseline.  Returns
+    None if the `cryptography` package is missing."""
+    try:
+        from concurrent.futures import ThreadPoolExecutor
+
+        from cryptography.hazmat.primitives.ciphers import Cipher, algorithms, modes
+    except ImportError:
+        return None
+    threads = os.cpu_count() or 1
+    n = 1 << 22
+    rng = np.random.default_rng(SEED + 2)
+    p = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    x = p ^ np.frombuffer(iv, np.uint8)
+    parts = np.array_split(x, threads)
+
+    def enc(part):
+        e = Cipher(algorithms.AES(key), modes.ECB()).encryptor()
+        return e.update(part.tobytes()) + e.finalize()
+
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        list(pool.map(enc, parts))  # warm
+        t0 = time.perf_counter()
+        reps = 0
+        while time.perf_counter() - t0 < budget_s:
+            list(pool.map(enc, parts))
+            reps += 1
+        sec = (time.perf_counter() - t0) / reps
+    return {"value": round(n * BYTES_PER_BLOCK / sec / 1e9, 3), "unit": "GB/s", "cores": threads,
+            "sample": f"{n} blocks, AES-128-ECB of P^IV via OpenSSL (cryptography), {threads} threads"}
+
+
 def run_reference_impl(args):
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
@@ -633,8 +666,10 @@ def main():
     }
 
     cpu = None
+    openssl = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(key, iv, args.cpu_seconds)
+        openssl = openssl_rate(key, iv)
 
     if rank == 0:
         line = {
@@ -651,6 +686,7 @@ def main():
                        "host_cpus": (f"{len(numa_cpus)} CPUs local to the GPU" if numa_cpus else "all"),
                        **inp["meta"]},
             "gpu_launches": launches, "roofline": roofline, "e2e": e2e, "e2e_dropin": dropin, "cpu_baseline": cpu,
+            "cpu_openssl": openssl,
             "clocks": clocks,
             "decrypt_gbs_per_gpu": round(dec_gbs, 2), "verified": verified, "verification": check,
             "step_ms": [round(x, 4) for x in ms],
