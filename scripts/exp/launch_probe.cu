@@ -14,6 +14,11 @@ __global__ void __launch_bounds__(1024, 1) fill_k(const uint32_t* compact, int* 
   if (threadIdx.x == 9999) sink[0] = smem[0];
 }
 __global__ void small_k(int* sink) { if (threadIdx.x == 9999) sink[0] = 1; }
+__global__ void __launch_bounds__(256, 1) fill256_k(const uint32_t* compact, int* sink) {
+  extern __shared__ __align__(1024) char smem[];
+  fill_tables(smem, compact);
+  if (threadIdx.x == 9999) sink[0] = smem[0];
+}
 template <typename F>
 float timeit(F f) {
   cudaEvent_t a, b;
@@ -36,5 +41,8 @@ int main() {
   printf("148 x 1024 thr, 192 KiB smem, empty:  %.2f us\n", timeit([&] { empty_k<<<148, 1024, kSmemBytes>>>(sink); }));
   printf("148 x 1024 thr, 192 KiB smem, fill:   %.2f us\n", timeit([&] { fill_k<<<148, 1024, kSmemBytes>>>(tab, sink); }));
   printf("64 x 1024 thr, 192 KiB smem, fill:    %.2f us\n", timeit([&] { fill_k<<<64, 1024, kSmemBytes>>>(tab, sink); }));
+  cudaFuncSetAttribute(fill256_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  printf("148 x 256 thr, 192 KiB smem, fill:    %.2f us\n", timeit([&] { fill256_k<<<148, 256, kSmemBytes>>>(tab, sink); }));
+  printf("148 x 256 thr, no smem, empty:        %.2f us\n", timeit([&] { empty_k<<<148, 256, 0>>>(sink); }));
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
 }
