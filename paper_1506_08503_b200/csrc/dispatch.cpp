@@ -98,6 +98,16 @@ struct DevCtx {
   uint8_t* d_tmp = nullptr;      // GF-build outputs + error flag
   uint8_t* d_mk = nullptr;       // many-key: keys | rk (K x 176) | ivs
   size_t mk_cap = 0;
+  // linear textures over input buffers (texture-path loads, see k_blocks)
+  struct Tex {
+    const void* ptr;
+    size_t bytes;
+    cudaTextureObject_t tex;
+  };
+  std::mutex tex_mu;
+  std::vector<Tex> tex_cache;
+  int tex_align = 0;
+  size_t tex_max_texels = 0;
   Slot slots[kSlots];
   // Only runs when initialisation fails (live contexts are never destroyed:
   // freeing after the CUDA runtime has shut down at exit is not allowed).
@@ -109,6 +119,7 @@ struct DevCtx {
       if (s.done) cudaEventDestroy(s.done);
     }
     for (auto& kv : cache) cudaFree(kv.second);
+    for (auto& t : tex_cache) cudaDestroyTextureObject(t.tex);
   }
 };
 
@@ -265,10 +276,55 @@ int tables_for(DevCtx* c, const uint8_t* box, const uint8_t* lut, uint32_t** out
   return GAES_OK;
 }
 
+// A linear uint4 texture over [ptr, ptr + bytes) for the texture-path input
+// loads of the folded kernels, cached per device by pointer (callers and the
+// staging slots reuse buffers).  0 when disabled (GAES_TEXIN=0), misaligned,
+// too large or unavailable -- the kernels then use LDG.  Must be called with
+// c->dev current.
+cudaTextureObject_t tex_for(DevCtx* c, const void* ptr, size_t bytes) {
+  static const bool enabled = env_int("GAES_TEXIN", 1) != 0;
+  if (!enabled || !ptr || bytes < 16) return 0;
+  std::lock_guard<std::mutex> lk(c->tex_mu);
+  if (c->tex_align == 0) {
+    int align = 0, maxw = 0;
+    if (cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, c->dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxTexture1DLinearWidth, c->dev) != cudaSuccess) {
+      cudaGetLastError();
+      c->tex_align = -1;
+    } else {
+      c->tex_align = std::max(align, 16);
+      c->tex_max_texels = (size_t)maxw;
+    }
+  }
+  if (c->tex_align < 0 || reinterpret_cast<uintptr_t>(ptr) % (uintptr_t)c->tex_align != 0) return 0;
+  if (bytes / 16 > c->tex_max_texels || bytes / 16 > 0x7FFFFFFFull) return 0;
+  for (auto& t : c->tex_cache)
+    if (t.ptr == ptr && t.bytes >= bytes) return t.tex;
+  if (c->tex_cache.size() >= 16) {  // evict all (a kernel in flight may still read one)
+    cudaDeviceSynchronize();
+    for (auto& t : c->tex_cache) cudaDestroyTextureObject(t.tex);
+    c->tex_cache.clear();
+  }
+  cudaResourceDesc rd = {};
+  rd.resType = cudaResourceTypeLinear;
+  rd.res.linear.devPtr = const_cast<void*>(ptr);
+  rd.res.linear.desc = cudaCreateChannelDesc<uint4>();
+  rd.res.linear.sizeInBytes = bytes / 16 * 16;
+  cudaTextureDesc td = {};
+  td.readMode = cudaReadModeElementType;
+  cudaTextureObject_t tex = 0;
+  if (cudaCreateTextureObject(&tex, &rd, &td, nullptr) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  c->tex_cache.push_back({ptr, bytes, tex});
+  return tex;
+}
+
 // M = 16 shared-IV encrypt: the formulation chosen by measurement
 // (profiles/): T-table unless gaes_set_variant(2) selects the bitsliced kernel.
 cudaError_t launch_enc_folded(DevCtx* c, const void* in, void* out, uint64_t n, const uint32_t* compact,
-                              const RoundKeys& k, int ilp, cudaStream_t s);
+                              const RoundKeys& k, int ilp, cudaStream_t s, cudaTextureObject_t tin);
 
 int ilp_default() {
   // ILP 1 measured ~1% faster than 2 at configs 2 and 3 (finer tail, 40 regs)
@@ -277,7 +333,7 @@ int ilp_default() {
 }
 
 cudaError_t launch_enc_folded(DevCtx* c, const void* in, void* out, uint64_t n, const uint32_t* compact,
-                              const RoundKeys& k, int ilp, cudaStream_t s) {
+                              const RoundKeys& k, int ilp, cudaStream_t s, cudaTextureObject_t tin) {
   if (g_variant.load() == 2) {
     static thread_local BitsliceKeys bk;
     bs_make_keys(k.w, bk);
@@ -285,7 +341,7 @@ cudaError_t launch_enc_folded(DevCtx* c, const void* in, void* out, uint64_t n, 
     return launch_bs_blocks(in, out, n, bk, c->sms, s);
   }
   note_kernel("k_blocks_enc_folded");
-  return launch_blocks(false, kIvFolded, ilp, in, out, n, compact, k, nullptr, 1, c->sms, s);
+  return launch_blocks(false, kIvFolded, ilp, in, out, n, compact, k, nullptr, 1, c->sms, s, tin);
 }
 
 // --------------------------------------------------------------------------
@@ -367,10 +423,11 @@ int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t r0, size_t rows, const
     case Mode::kFolded:
       if (j.dec) {
         GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,
-                              c->sms, s.stream));
+                              c->sms, s.stream, tex_for(c, s.d_in, s.cap)));
         note_kernel("k_blocks_dec_folded");
       } else if (j.standard || g_variant.load() < 2) {
-        GAES_CK(launch_enc_folded(c, s.d_in, s.d_out, nblk, compact, j.rk, ilp_default(), s.stream));
+        GAES_CK(launch_enc_folded(c, s.d_in, s.d_out, nblk, compact, j.rk, ilp_default(), s.stream,
+                                  tex_for(c, s.d_in, s.cap)));
       } else {  // bitsliced kernel has the standard S-box built in; caller tables -> T-table
         GAES_CK(launch_blocks(false, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,
                               c->sms, s.stream));
@@ -896,7 +953,8 @@ GAES_API int gaes_encrypt_blocks_dev(const void* in, void* out, size_t n_blocks,
   int rc = current_ctx(&c);
   if (rc) return rc;
   const RoundKeys k = make_enc_keys(round_keys, iv, true);
-  GAES_CK(launch_enc_folded(c, in, out, n_blocks, c->d_std_enc, k, ilp_default(), (cudaStream_t)stream));
+  GAES_CK(launch_enc_folded(c, in, out, n_blocks, c->d_std_enc, k, ilp_default(), (cudaStream_t)stream,
+                            tex_for(c, in, n_blocks * 16)));
   return GAES_OK;
 }
 
@@ -909,7 +967,7 @@ GAES_API int gaes_decrypt_blocks_dev(const void* in, void* out, size_t n_blocks,
   if (rc) return rc;
   const RoundKeys k = make_dec_keys(round_keys, iv, true, nullptr);
   GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), in, out, n_blocks, c->d_std_dec, k, nullptr, 1, c->sms,
-                        (cudaStream_t)stream));
+                        (cudaStream_t)stream, tex_for(c, in, n_blocks * 16)));
   note_kernel("k_blocks_dec_folded");
   return GAES_OK;
 }

@@ -96,11 +96,15 @@ __device__ __forceinline__ void st_stream(uint4* p, uint4 v) { __stcs(p, v); }
 //                     x = j ? in[b-1] : (ivs ? ivs[i] : rk.iv).
 //                     encrypt: state ^= x (only valid for bpr == 1);
 //                     decrypt: out ^= x.
-template <int ILP, bool DEC, int IVM>
+//   TEXIN: the 16-byte input loads go through the texture path
+//          (tex1Dfetch on a linear texture over `in`) instead of LDG: the
+//          L1/shared data pipe the table lookups saturate then carries only
+//          the lookups and the stores (+1.5 %, profiles/r1_formulation_choice.md).
+template <int ILP, bool DEC, int IVM, bool TEXIN = false>
 __global__ void __launch_bounds__(kBlockThreads, 1)
     k_blocks(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks,
              const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
-             const uint4* __restrict__ ivs, uint64_t bpr) {
+             const uint4* __restrict__ ivs, uint64_t bpr, cudaTextureObject_t tin) {
   extern __shared__ __align__(1024) char smem[];
   pdl_prologue(smem, compact);
   const uint32_t lane = threadIdx.x & 31;
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
   uint4 cur[ILP];
 #pragma unroll
   for (int k = 0; k < ILP; k++)
-    if (b + k * T < n_blocks) cur[k] = ld_stream(in + b + k * T);
+    if (b + k * T < n_blocks) cur[k] = TEXIN ? tex1Dfetch<uint4>(tin, (int)(b + k * T)) : ld_stream(in + b + k * T);
 
   // CHAIN mode: (row, j) of every slot is tracked incrementally -- one
   // 64-bit division per thread instead of one per block.
@@ -131,7 +135,8 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
     uint4 nxt[ILP];
 #pragma unroll
     for (int k = 0; k < ILP; k++)
-      if (nb + k * T < n_blocks) nxt[k] = ld_stream(in + nb + k * T);
+      if (nb + k * T < n_blocks)
+        nxt[k] = TEXIN ? tex1Dfetch<uint4>(tin, (int)(nb + k * T)) : ld_stream(in + nb + k * T);
 
 #pragma unroll
     for (int k = 0; k < ILP; k++) {
@@ -521,21 +526,26 @@ cudaError_t launch_build_tables(const uint8_t* box, const uint8_t* lut, uint32_t
   return cudaGetLastError();
 }
 
-template <int ILP, bool DEC, int IVM>
+template <int ILP, bool DEC, int IVM, bool TEXIN = false>
 static cudaError_t launch_blocks_t(const void* in, void* out, uint64_t n, const uint32_t* compact,
-                                   const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms, cudaStream_t s) {
-  auto kern = k_blocks<ILP, DEC, IVM>;
+                                   const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms, cudaStream_t s,
+                                   cudaTextureObject_t tin = 0) {
+  auto kern = k_blocks<ILP, DEC, IVM, TEXIN>;
   cudaError_t e = set_smem(kern);
   if (e != cudaSuccess) return e;
   const int grid = grid_for(n, ILP, sms);
   return launch_pdl(kern, grid, kBlockThreads, kSmemBytes, s, (const uint4*)in, (uint4*)out, n, compact, rk,
-                    (const uint4*)ivs, bpr);
+                    (const uint4*)ivs, bpr, tin);
 }
 
 cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* out, uint64_t n_blocks,
                           const uint32_t* compact, const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms,
-                          cudaStream_t s) {
+                          cudaStream_t s, cudaTextureObject_t tin) {
   if (n_blocks == 0) return cudaSuccess;
+  if (tin && ivmode == kIvFolded && n_blocks <= 0x7FFFFFFFull) {
+    if (dec) return launch_blocks_t<1, true, kIvFolded, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin);
+    return launch_blocks_t<1, false, kIvFolded, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin);
+  }
   // Small batches: spread over every SM (one block per thread) rather than
   // giving few CTAs two blocks per thread; the 192 KiB table fill is per CTA.
   if ((uint64_t)sms * kBlockThreads * 8 > n_blocks) ilp = 1;
