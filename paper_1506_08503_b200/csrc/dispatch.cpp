@@ -283,7 +283,7 @@ int tables_for(DevCtx* c, const uint8_t* box, const uint8_t* lut, uint32_t** out
 // c->dev current.
 cudaTextureObject_t tex_for(DevCtx* c, const void* ptr, size_t bytes) {
   static const bool enabled = env_int("GAES_TEXIN", 1) != 0;
-  if (!enabled || !ptr || bytes < 16) return 0;
+  if (!enabled) return 0;
   std::lock_guard<std::mutex> lk(c->tex_mu);
   if (c->tex_align == 0) {
     int align = 0, maxw = 0;
@@ -296,6 +296,7 @@ cudaTextureObject_t tex_for(DevCtx* c, const void* ptr, size_t bytes) {
       c->tex_max_texels = (size_t)maxw;
     }
   }
+  if (!ptr || bytes < 16) return 0;
   if (c->tex_align < 0 || reinterpret_cast<uintptr_t>(ptr) % (uintptr_t)c->tex_align != 0) return 0;
   if (bytes / 16 > c->tex_max_texels || bytes / 16 > 0x7FFFFFFFull) return 0;
   for (auto& t : c->tex_cache)
@@ -319,6 +320,30 @@ cudaTextureObject_t tex_for(DevCtx* c, const void* ptr, size_t bytes) {
   }
   c->tex_cache.push_back({ptr, bytes, tex});
   return tex;
+}
+
+// Largest launch (in 16-byte blocks) that a texture can cover on this
+// device; device-API calls above it are cut into segments so every segment
+// keeps the texture-path loads.  0 = textures unavailable.
+size_t tex_segment_blocks(DevCtx* c) {
+  tex_for(c, nullptr, 0);  // no-op; attributes are queried below on first use
+  std::lock_guard<std::mutex> lk(c->tex_mu);
+  if (c->tex_align == 0) return 0;  // not queried yet: caller falls back to one launch
+  if (c->tex_align < 0) return 0;
+  size_t seg = std::min<size_t>(c->tex_max_texels, 0x7FFFFFFFull);
+  return seg & ~((size_t)(1 << 20) - 1);
+}
+
+// Runs fn(offset, count) over [0, n) in texture-sized segments.
+template <typename F>
+int for_segments(DevCtx* c, size_t n, F&& fn) {
+  size_t seg = tex_segment_blocks(c);
+  if (seg == 0 || n <= seg) return fn((size_t)0, n);
+  for (size_t off = 0; off < n; off += seg) {
+    int rc = fn(off, std::min(seg, n - off));
+    if (rc) return rc;
+  }
+  return GAES_OK;
 }
 
 // M = 16 shared-IV encrypt: the formulation chosen by measurement
@@ -448,7 +473,7 @@ int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t r0, size_t rows, const
       const size_t kb = j.n_keys * 16, rkb = j.n_keys * 176;
       GAES_CK(launch_many_key(j.dec, s.d_in, s.d_out, nblk, j.first + r0, j.bpk, compact,
                               c->d_mk + kb + (j.dec ? rkb : 0), j.mk_ivs ? c->d_mk + kb + 2 * rkb : nullptr, c->sms,
-                              s.stream));
+                              s.stream, tex_for(c, s.d_in, s.cap)));
       note_kernel(j.dec ? "k_many_key_dec" : "k_many_key_enc");
       break;
     }
@@ -953,9 +978,12 @@ GAES_API int gaes_encrypt_blocks_dev(const void* in, void* out, size_t n_blocks,
   int rc = current_ctx(&c);
   if (rc) return rc;
   const RoundKeys k = make_enc_keys(round_keys, iv, true);
-  GAES_CK(launch_enc_folded(c, in, out, n_blocks, c->d_std_enc, k, ilp_default(), (cudaStream_t)stream,
-                            tex_for(c, in, n_blocks * 16)));
-  return GAES_OK;
+  return for_segments(c, n_blocks, [&](size_t off, size_t cnt) {
+    const uint4* i = static_cast<const uint4*>(in) + off;
+    GAES_CK(launch_enc_folded(c, i, static_cast<uint4*>(out) + off, cnt, c->d_std_enc, k, ilp_default(),
+                              (cudaStream_t)stream, tex_for(c, i, cnt * 16)));
+    return GAES_OK;
+  });
 }
 
 GAES_API int gaes_decrypt_blocks_dev(const void* in, void* out, size_t n_blocks, const uint8_t round_keys[176],
@@ -966,10 +994,13 @@ GAES_API int gaes_decrypt_blocks_dev(const void* in, void* out, size_t n_blocks,
   int rc = current_ctx(&c);
   if (rc) return rc;
   const RoundKeys k = make_dec_keys(round_keys, iv, true, nullptr);
-  GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), in, out, n_blocks, c->d_std_dec, k, nullptr, 1, c->sms,
-                        (cudaStream_t)stream, tex_for(c, in, n_blocks * 16)));
-  note_kernel("k_blocks_dec_folded");
-  return GAES_OK;
+  return for_segments(c, n_blocks, [&](size_t off, size_t cnt) {
+    const uint4* i = static_cast<const uint4*>(in) + off;
+    GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), i, static_cast<uint4*>(out) + off, cnt, c->d_std_dec, k,
+                          nullptr, 1, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16)));
+    note_kernel("k_blocks_dec_folded");
+    return GAES_OK;
+  });
 }
 
 GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m, const void* ivs_dev,
@@ -1030,10 +1061,13 @@ GAES_API int gaes_many_key_encrypt_dev(const void* in, void* out, size_t blocks_
   DevCtx* c = nullptr;
   int rc = current_ctx(&c);
   if (rc) return rc;
-  GAES_CK(launch_many_key(false, in, out, blocks_per_key * k, 0, blocks_per_key, c->d_std_enc, rk_enc, ivs_dev, c->sms,
-                          (cudaStream_t)stream));
-  note_kernel("k_many_key_enc");
-  return GAES_OK;
+  return for_segments(c, blocks_per_key * k, [&](size_t off, size_t cnt) {
+    const uint4* i = static_cast<const uint4*>(in) + off;
+    GAES_CK(launch_many_key(false, i, static_cast<uint4*>(out) + off, cnt, off, blocks_per_key, c->d_std_enc, rk_enc,
+                            ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16)));
+    note_kernel("k_many_key_enc");
+    return GAES_OK;
+  });
 }
 
 GAES_API int gaes_many_key_decrypt_dev(const void* in, void* out, size_t blocks_per_key, size_t k,
@@ -1043,10 +1077,13 @@ GAES_API int gaes_many_key_decrypt_dev(const void* in, void* out, size_t blocks_
   DevCtx* c = nullptr;
   int rc = current_ctx(&c);
   if (rc) return rc;
-  GAES_CK(launch_many_key(true, in, out, blocks_per_key * k, 0, blocks_per_key, c->d_std_dec, rk_dec, ivs_dev, c->sms,
-                          (cudaStream_t)stream));
-  note_kernel("k_many_key_dec");
-  return GAES_OK;
+  return for_segments(c, blocks_per_key * k, [&](size_t off, size_t cnt) {
+    const uint4* i = static_cast<const uint4*>(in) + off;
+    GAES_CK(launch_many_key(true, i, static_cast<uint4*>(out) + off, cnt, off, blocks_per_key, c->d_std_dec, rk_dec,
+                            ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16)));
+    note_kernel("k_many_key_dec");
+    return GAES_OK;
+  });
 }
 
 }  // extern "C"

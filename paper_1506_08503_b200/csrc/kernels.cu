@@ -367,11 +367,11 @@ __global__ void k_expand_keys(const uint8_t* __restrict__ keys, uint64_t k, cons
 // may cut chunks anywhere).  Round keys live in registers and are reloaded
 // only when a thread's walk through its CTA's contiguous range crosses into
 // the next key's blocks.
-template <bool DEC>
+template <bool DEC, bool TEXIN = false>
 __global__ void __launch_bounds__(kManyKeyThreads, 1)
     k_many_key(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks, uint64_t first,
                uint64_t bpk, const uint32_t* __restrict__ compact, const uint4* __restrict__ rks,
-               const uint4* __restrict__ ivs) {
+               const uint4* __restrict__ ivs, cudaTextureObject_t tin) {
   extern __shared__ __align__(1024) char smem[];
   pdl_prologue(smem, compact);
   const uint32_t lb = (threadIdx.x & 31) * 4;
@@ -397,11 +397,11 @@ __global__ void __launch_bounds__(kManyKeyThreads, 1)
     rk.w[0] ^= iv.x; rk.w[1] ^= iv.y; rk.w[2] ^= iv.z; rk.w[3] ^= iv.w;
   };
   load_key(key);
-  uint4 cur = ld_stream(in + b);
+  uint4 cur = TEXIN ? tex1Dfetch<uint4>(tin, (int)b) : ld_stream(in + b);
   while (b < hi) {
     const uint64_t nb = b + blockDim.x;
     uint4 nxt = cur;
-    if (nb < hi) nxt = ld_stream(in + nb);
+    if (nb < hi) nxt = TEXIN ? tex1Dfetch<uint4>(tin, (int)nb) : ld_stream(in + nb);
     if (b >= key_end) {
       key = (first + b) / bpk;
       key_end = (key + 1) * bpk - first;
@@ -614,14 +614,17 @@ cudaError_t launch_expand_keys(const uint8_t* keys, uint64_t k, const uint32_t* 
 }
 
 cudaError_t launch_many_key(bool dec, const void* in, void* out, uint64_t n_blocks, uint64_t first, uint64_t bpk,
-                            const uint32_t* compact, const void* rks, const void* ivs, int sms, cudaStream_t s) {
+                            const uint32_t* compact, const void* rks, const void* ivs, int sms, cudaStream_t s,
+                            cudaTextureObject_t tin) {
   if (bpk == 0 || n_blocks == 0) return cudaSuccess;
-  cudaError_t e = dec ? set_smem(k_many_key<true>) : set_smem(k_many_key<false>);
+  if (n_blocks > 0x7FFFFFFFull) tin = 0;
+  auto kern = dec ? (tin ? k_many_key<true, true> : k_many_key<true, false>)
+                  : (tin ? k_many_key<false, true> : k_many_key<false, false>);
+  cudaError_t e = set_smem(kern);
   if (e != cudaSuccess) return e;
   const int grid = grid_for(n_blocks, 1, sms, kManyKeyThreads);
-  return launch_pdl(dec ? k_many_key<true> : k_many_key<false>, grid, kManyKeyThreads, kSmemBytes, s,
-                    (const uint4*)in, (uint4*)out, n_blocks, first, bpk, compact, (const uint4*)rks,
-                    (const uint4*)ivs);
+  return launch_pdl(kern, grid, kManyKeyThreads, kSmemBytes, s, (const uint4*)in, (uint4*)out, n_blocks, first, bpk,
+                    compact, (const uint4*)rks, (const uint4*)ivs, tin);
 }
 
 }  // namespace gaes

@@ -35,6 +35,7 @@ cudaError_t launch_round_probe(const uint32_t* compact, const RoundKeys& rk, uin
 cudaError_t launch_expand_keys(const uint8_t* keys, uint64_t k, const uint32_t* compact_enc, uint8_t* rk_enc,
                                uint8_t* rk_dec, cudaStream_t s);
 cudaError_t launch_many_key(bool dec, const void* in, void* out, uint64_t n_blocks, uint64_t first, uint64_t bpk,
-                            const uint32_t* compact, const void* rks, const void* ivs, int sms, cudaStream_t s);
+                            const uint32_t* compact, const void* rks, const void* ivs, int sms, cudaStream_t s,
+                            cudaTextureObject_t tin = 0);
 
 }  // namespace gaes
