@@ -461,7 +461,7 @@ int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t r0, size_t rows, const
       break;
     case Mode::kChain:
       GAES_CK(launch_blocks(j.dec, kIvChain, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk,
-                            j.ivs ? s.d_iv : nullptr, bpr, c->sms, s.stream));
+                            j.ivs ? s.d_iv : nullptr, bpr, c->sms, s.stream, tex_for(c, s.d_in, s.cap)));
       note_kernel(j.dec ? "k_blocks_dec_chain" : "k_blocks_enc_chain");
       break;
     case Mode::kEncRows:
@@ -1016,7 +1016,7 @@ GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m,
   const RoundKeys k = make_enc_keys(round_keys, iv, false);
   if (bpr == 1) {
     GAES_CK(launch_blocks(false, kIvChain, ilp_default(), in, out, n, c->d_std_enc, k, ivs_dev, 1, c->sms,
-                          (cudaStream_t)stream));
+                          (cudaStream_t)stream, tex_for(c, in, n * 16)));
     note_kernel("k_blocks_enc_chain");
   } else {
     GAES_CK(launch_cbc_enc_rows(in, out, n, bpr, c->d_std_enc, k, ivs_dev, c->sms, (cudaStream_t)stream));
@@ -1037,7 +1037,7 @@ GAES_API int gaes_cbc_decrypt_dev(const void* in, void* out, size_t n, size_t m,
   if (bpr == 1 && !ivs_dev) return gaes_decrypt_blocks_dev(in, out, n, round_keys, iv, stream);
   const RoundKeys k = make_dec_keys(round_keys, iv, false, nullptr);
   GAES_CK(launch_blocks(true, kIvChain, ilp_default(), in, out, n * bpr, c->d_std_dec, k, ivs_dev, bpr, c->sms,
-                        (cudaStream_t)stream));
+                        (cudaStream_t)stream, tex_for(c, in, n * bpr * 16)));
   note_kernel("k_blocks_dec_chain");
   return GAES_OK;
 }

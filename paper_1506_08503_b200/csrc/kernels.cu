@@ -99,7 +99,8 @@ __device__ __forceinline__ void st_stream(uint4* p, uint4 v) { __stcs(p, v); }
 //   TEXIN: the 16-byte input loads go through the texture path
 //          (tex1Dfetch on a linear texture over `in`) instead of LDG: the
 //          L1/shared data pipe the table lookups saturate then carries only
-//          the lookups and the stores (+1.5 %, profiles/r1_formulation_choice.md).
+//          the lookups and the stores (+1.0-1.2 % in bench.py,
+//          profiles/r1_formulation_choice.md).
 template <int ILP, bool DEC, int IVM, bool TEXIN = false>
 __global__ void __launch_bounds__(kBlockThreads, 1)
     k_blocks(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks,
@@ -542,9 +543,13 @@ cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* o
                           const uint32_t* compact, const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms,
                           cudaStream_t s, cudaTextureObject_t tin) {
   if (n_blocks == 0) return cudaSuccess;
-  if (tin && ivmode == kIvFolded && n_blocks <= 0x7FFFFFFFull) {
-    if (dec) return launch_blocks_t<1, true, kIvFolded, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin);
-    return launch_blocks_t<1, false, kIvFolded, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin);
+  if (tin && n_blocks <= 0x7FFFFFFFull) {
+    if (ivmode == kIvFolded) {
+      if (dec) return launch_blocks_t<1, true, kIvFolded, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin);
+      return launch_blocks_t<1, false, kIvFolded, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin);
+    }
+    if (dec) return launch_blocks_t<1, true, kIvChain, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin);
+    return launch_blocks_t<1, false, kIvChain, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin);
   }
   // Small batches: spread over every SM (one block per thread) rather than
   // giving few CTAs two blocks per thread; the 192 KiB table fill is per CTA.
