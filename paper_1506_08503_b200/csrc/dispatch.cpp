@@ -466,7 +466,7 @@ int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t r0, size_t rows, const
       break;
     case Mode::kEncRows:
       GAES_CK(launch_cbc_enc_rows(s.d_in, s.d_out, rows, bpr, compact, j.rk, j.ivs ? s.d_iv : nullptr, c->sms,
-                                  s.stream));
+                                  s.stream, tex_for(c, s.d_in, s.cap)));
       note_kernel("k_cbc_enc_rows");
       break;
     case Mode::kManyKey: {
@@ -1019,7 +1019,17 @@ GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m,
                           (cudaStream_t)stream, tex_for(c, in, n * 16)));
     note_kernel("k_blocks_enc_chain");
   } else {
-    GAES_CK(launch_cbc_enc_rows(in, out, n, bpr, c->d_std_enc, k, ivs_dev, c->sms, (cudaStream_t)stream));
+    // segments of whole rows, each inside one texture
+    const size_t seg_blocks = tex_segment_blocks(c);
+    const size_t seg_rows = seg_blocks >= bpr ? seg_blocks / bpr : n;
+    const uint8_t* i8 = static_cast<const uint8_t*>(in);
+    uint8_t* o8 = static_cast<uint8_t*>(out);
+    const uint8_t* v8 = static_cast<const uint8_t*>(ivs_dev);
+    for (size_t r = 0; r < n; r += seg_rows) {
+      const size_t cnt = std::min(seg_rows, n - r);
+      GAES_CK(launch_cbc_enc_rows(i8 + r * m, o8 + r * m, cnt, bpr, c->d_std_enc, k, v8 ? v8 + r * 16 : nullptr,
+                                  c->sms, (cudaStream_t)stream, tex_for(c, i8 + r * m, cnt * m)));
+    }
     note_kernel("k_cbc_enc_rows");
   }
   return GAES_OK;

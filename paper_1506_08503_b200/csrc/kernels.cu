@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -201,12 +202,14 @@ __device__ __forceinline__ void st_pair(uint4* p, const uint4& a, const uint4& b
 // CBC encrypt along rows: thread per row, serial chain (_kernel.pyx:29-54).
 // Lanes walk 32 different rows (stride M), so every warp access touches 32
 // cache lines; PAIRS moves two blocks per access (32-byte aligned grids),
-// halving the L1 wavefronts per block.
-template <bool PAIRS>
+// halving the L1 wavefronts per block.  TEXIN fetches the plaintext through
+// the texture path instead (its own pipe: the strided loads stop competing
+// with the table lookups for L1 data-pipe wavefronts).
+template <bool PAIRS, bool TEXIN>
 __global__ void __launch_bounds__(kBlockThreads, 1)
     k_cbc_enc_rows(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_rows, uint64_t bpr,
                    const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
-                   const uint4* __restrict__ ivs) {
+                   const uint4* __restrict__ ivs, cudaTextureObject_t tin) {
   extern __shared__ __align__(1024) char smem[];
   pdl_prologue(smem, compact);
   const uint32_t lb = (threadIdx.x & 31) * 4;
@@ -217,15 +220,20 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
     encrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
     c = make_uint4(s0, s1, s2, s3);
   };
+  auto load = [&](uint64_t i) { return TEXIN ? tex1Dfetch<uint4>(tin, (int)i) : __ldg(in + i); };
+  auto load_pair = [&](uint64_t i) {
+    if (TEXIN) return Pair{tex1Dfetch<uint4>(tin, (int)i), tex1Dfetch<uint4>(tin, (int)(i + 1))};
+    return ld_pair(in + i);
+  };
   for (uint64_t row = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n_rows; row += T) {
     uint4 c = ivs ? __ldg(ivs + row) : make_uint4(rk.iv[0], rk.iv[1], rk.iv[2], rk.iv[3]);
-    const uint4* src = in + row * bpr;
+    const uint64_t src = row * bpr;
     uint4* dst = out + row * bpr;
     if (PAIRS) {
       const uint64_t pairs = bpr / 2;
-      Pair p = ld_pair(src);
+      Pair p = load_pair(src);
       for (uint64_t q = 0; q < pairs; q++) {
-        const Pair pn = (q + 1 < pairs) ? ld_pair(src + 2 * q + 2) : p;
+        const Pair pn = (q + 1 < pairs) ? load_pair(src + 2 * q + 2) : p;
         uint4 c0 = c;
         enc(p.a, c0);
         uint4 c1 = c0;
@@ -235,15 +243,15 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
         p = pn;
       }
       if (bpr & 1) {  // odd tail block
-        enc(__ldg(src + bpr - 1), c);
+        enc(load(src + bpr - 1), c);
         st_stream(dst + bpr - 1, c);
       }
     } else {
       // cached loads: the second 16 B of each 32-B sector is consumed one
       // iteration later and should hit L1
-      uint4 p = __ldg(src);
+      uint4 p = load(src);
       for (uint64_t j = 0; j < bpr; j++) {
-        const uint4 pn = (j + 1 < bpr) ? __ldg(src + j + 1) : p;
+        const uint4 pn = (j + 1 < bpr) ? load(src + j + 1) : p;
         enc(p, c);
         st_stream(dst + j, c);
         p = pn;
@@ -563,17 +571,39 @@ cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* o
   return cudaErrorInvalidValue;
 }
 
+// Row-CBC geometry: a thread owns whole rows, so the launch is sized in
+// whole waves of rows -- e.g. 2^18 rows over 148 x 1024 threads would leave
+// the second wave 73% full; 148 x 896 threads run two full waves instead
+// (626 -> 714 GB/s at 64-block rows).
+static void rows_geometry(uint64_t n_rows, int sms, int* grid, int* threads) {
+  const uint64_t cap = (uint64_t)sms * kBlockThreads;
+  const uint64_t waves = (n_rows + cap - 1) / cap;
+  const uint64_t per_wave = (n_rows + waves - 1) / waves;
+  uint64_t t = (per_wave + sms - 1) / sms;
+  t = std::max<uint64_t>(128, (t + 31) & ~(uint64_t)31);
+  t = std::min<uint64_t>(t, kBlockThreads);
+  *threads = (int)t;
+  *grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(sms, (per_wave + t - 1) / t));
+}
+
 cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint64_t bpr, const uint32_t* compact,
-                                const RoundKeys& rk, const void* ivs, int sms, cudaStream_t s) {
+                                const RoundKeys& rk, const void* ivs, int sms, cudaStream_t s,
+                                cudaTextureObject_t tin) {
   if (n_rows == 0) return cudaSuccess;
   const bool pairs = bpr >= 2 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 31) == 0 &&
                      (bpr % 2 == 0);
-  auto kern = pairs ? k_cbc_enc_rows<true> : k_cbc_enc_rows<false>;
+  // texture loads measured +1.5% at 2-4 blocks per row and neutral to -2%
+  // from 16 up (scattered 16-byte fetches, one line per lane, are not cheaper
+  // on the TEX pipe than LDG.256)
+  if (n_rows * bpr > 0x7FFFFFFFull || bpr > 8) tin = 0;
+  auto kern = tin ? (pairs ? k_cbc_enc_rows<true, true> : k_cbc_enc_rows<false, true>)
+                  : (pairs ? k_cbc_enc_rows<true, false> : k_cbc_enc_rows<false, false>);
   cudaError_t e = set_smem(kern);
   if (e != cudaSuccess) return e;
-  const int grid = grid_for(n_rows, 1, sms);
-  return launch_pdl(kern, grid, kBlockThreads, kSmemBytes, s, (const uint4*)in, (uint4*)out, n_rows, bpr, compact,
-                    rk, (const uint4*)ivs);
+  int grid = 0, threads = 0;
+  rows_geometry(n_rows, sms, &grid, &threads);
+  return launch_pdl(kern, grid, threads, kSmemBytes, s, (const uint4*)in, (uint4*)out, n_rows, bpr, compact, rk,
+                    (const uint4*)ivs, tin);
 }
 
 cudaError_t launch_generic(bool dec, const uint8_t* data, const uint8_t* ivs, uint64_t n, uint64_t m,

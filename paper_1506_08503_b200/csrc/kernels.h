@@ -23,7 +23,8 @@ cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* o
                           const uint32_t* compact, const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms,
                           cudaStream_t s, cudaTextureObject_t tin = 0);
 cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint64_t bpr, const uint32_t* compact,
-                                const RoundKeys& rk, const void* ivs, int sms, cudaStream_t s);
+                                const RoundKeys& rk, const void* ivs, int sms, cudaStream_t s,
+                                cudaTextureObject_t tin = 0);
 cudaError_t launch_generic(bool dec, const uint8_t* data, const uint8_t* ivs, uint64_t n, uint64_t m,
                            const uint8_t* rk, const uint8_t* box, const uint8_t* lut, const uint8_t* perm,
                            uint8_t* out, int sms, cudaStream_t s);

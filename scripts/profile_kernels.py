@@ -1,6 +1,6 @@
 """Run one hot-path op a few times on cuda:0 (a small target for ncu).
 
-    python scripts/profile_kernels.py {encrypt,decrypt,bitsliced,manykey,cbc_rows,cbc_dec_rows} [log2_blocks]
+    python scripts/profile_kernels.py {encrypt,decrypt,bitsliced,manykey,cbc_rows,cbc_dec_rows} [log2_blocks] [bpr]
 """
 import sys
 
@@ -12,6 +12,7 @@ from paper_1506_08503_b200 import _lib, device  # noqa: E402
 
 op = sys.argv[1]
 n = 1 << int(sys.argv[2] if len(sys.argv) > 2 else 24)
+bpr = int(sys.argv[3]) if len(sys.argv) > 3 else 64  # blocks per row for the cbc_* ops
 rng = np.random.default_rng(2016)
 key, iv = rng.bytes(16), rng.bytes(16)
 rk = device.expand_key(key)
@@ -24,10 +25,10 @@ def run():
     elif op == "bitsliced":
         _lib.check(_lib.lib().gaes_set_variant(2))
         device.encrypt_blocks(x, rk, iv)
-    elif op == "cbc_rows":  # general-M CBC encrypt, 64-block rows
-        device.cbc_encrypt(x.view(n // 64, 64 * 16), rk, iv)
+    elif op == "cbc_rows":  # general-M CBC encrypt, bpr-block rows
+        device.cbc_encrypt(x.view(n // bpr, bpr * 16), rk, iv)
     elif op == "cbc_dec_rows":
-        device.cbc_decrypt(x.view(n // 64, 64 * 16), rk, iv)
+        device.cbc_decrypt(x.view(n // bpr, bpr * 16), rk, iv)
 
 
 if op == "manykey":
