@@ -98,14 +98,19 @@ struct DevCtx {
   uint8_t* d_tmp = nullptr;      // GF-build outputs + error flag
   uint8_t* d_mk = nullptr;       // many-key: keys | rk (K x 176) | ivs
   size_t mk_cap = 0;
-  // linear textures over input buffers (texture-path loads, see k_blocks)
+  // linear textures over input buffers (texture-path loads, see k_blocks),
+  // least-recently-used first; see tex_for
   struct Tex {
-    const void* ptr;
-    size_t bytes;
-    cudaTextureObject_t tex;
+    const void* ptr = nullptr;
+    size_t bytes = 0;
+    cudaTextureObject_t tex = 0;
+    cudaEvent_t last = nullptr;  // recorded after every launch that reads it
+    std::atomic<int> users{0};   // leases not yet enqueued
+    uint64_t stamp = 0;
   };
   std::mutex tex_mu;
-  std::vector<Tex> tex_cache;
+  std::vector<std::unique_ptr<Tex>> tex_cache;
+  uint64_t tex_clock = 0;
   int tex_align = 0;
   size_t tex_max_texels = 0;
   Slot slots[kSlots];
@@ -119,7 +124,10 @@ struct DevCtx {
       if (s.done) cudaEventDestroy(s.done);
     }
     for (auto& kv : cache) cudaFree(kv.second);
-    for (auto& t : tex_cache) cudaDestroyTextureObject(t.tex);
+    for (auto& t : tex_cache) {
+      cudaDestroyTextureObject(t->tex);
+      if (t->last) cudaEventDestroy(t->last);
+    }
   }
 };
 
@@ -276,35 +284,84 @@ int tables_for(DevCtx* c, const uint8_t* box, const uint8_t* lut, uint32_t** out
   return GAES_OK;
 }
 
-// A linear uint4 texture over [ptr, ptr + bytes) for the texture-path input
-// loads of the folded kernels, cached per device by pointer (callers and the
-// staging slots reuse buffers).  0 when disabled (GAES_TEXIN=0), misaligned,
-// too large or unavailable -- the kernels then use LDG.  Must be called with
-// c->dev current.
-cudaTextureObject_t tex_for(DevCtx* c, const void* ptr, size_t bytes) {
-  static const bool enabled = env_int("GAES_TEXIN", 1) != 0;
-  if (!enabled) return 0;
-  std::lock_guard<std::mutex> lk(c->tex_mu);
-  if (c->tex_align == 0) {
-    int align = 0, maxw = 0;
-    if (cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, c->dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxTexture1DLinearWidth, c->dev) != cudaSuccess) {
-      cudaGetLastError();
-      c->tex_align = -1;
-    } else {
-      c->tex_align = std::max(align, 16);
-      c->tex_max_texels = (size_t)maxw;
-    }
+// Texture limits of c->dev, queried once.  Must be called with c->tex_mu held.
+void query_tex_limits(DevCtx* c) {
+  if (c->tex_align != 0) return;
+  int align = 0, maxw = 0;
+  if (cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, c->dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxTexture1DLinearWidth, c->dev) != cudaSuccess) {
+    cudaGetLastError();
+    c->tex_align = -1;
+  } else {
+    c->tex_align = std::max(align, 16);
+    c->tex_max_texels = (size_t)maxw;
   }
-  if (!ptr || bytes < 16) return 0;
-  if (c->tex_align < 0 || reinterpret_cast<uintptr_t>(ptr) % (uintptr_t)c->tex_align != 0) return 0;
-  if (bytes / 16 > c->tex_max_texels || bytes / 16 > 0x7FFFFFFFull) return 0;
+}
+
+// A texture object lent to one launch.  It converts to the handle the
+// launcher takes; when the lease ends -- the end of the full expression that
+// enqueued the launch -- an event is recorded on the launch stream, so the
+// entry can later be evicted once exactly the kernels that read it are done.
+class TexLease {
+ public:
+  TexLease() = default;
+  TexLease(DevCtx::Tex* e, cudaStream_t s) : e_(e), s_(s) {}
+  TexLease(const TexLease&) = delete;
+  TexLease& operator=(const TexLease&) = delete;
+  ~TexLease() {
+    if (!e_) return;
+    cudaEventRecord(e_->last, s_);
+    e_->users.fetch_sub(1, std::memory_order_release);
+  }
+  operator cudaTextureObject_t() const { return e_ ? e_->tex : 0; }
+
+ private:
+  DevCtx::Tex* e_ = nullptr;
+  cudaStream_t s_ = nullptr;
+};
+
+// A linear uint4 texture over [ptr, ptr + bytes) for the texture-path input
+// loads, cached per device by pointer (callers and the staging slots reuse
+// buffers).  Empty (handle 0) when disabled (GAES_TEXIN=0), misaligned, too
+// large or unavailable -- the kernels then use LDG.  Must be called with
+// c->dev current and the lease used for one launch on `stream`.  At 64
+// entries the least recently used idle entry is evicted after waiting for
+// the launches that read it (its `last` event); entries lent out right now
+// are never evicted.
+TexLease tex_for(DevCtx* c, const void* ptr, size_t bytes, cudaStream_t stream) {
+  static const bool enabled = env_int("GAES_TEXIN", 1) != 0;
+  if (!enabled || !ptr || bytes < 16) return {};
+  std::lock_guard<std::mutex> lk(c->tex_mu);
+  query_tex_limits(c);
+  if (c->tex_align < 0 || reinterpret_cast<uintptr_t>(ptr) % (uintptr_t)c->tex_align != 0) return {};
+  if (bytes / 16 > c->tex_max_texels || bytes / 16 > 0x7FFFFFFFull) return {};
   for (auto& t : c->tex_cache)
-    if (t.ptr == ptr && t.bytes >= bytes) return t.tex;
-  if (c->tex_cache.size() >= 16) {  // evict all (a kernel in flight may still read one)
-    cudaDeviceSynchronize();
-    for (auto& t : c->tex_cache) cudaDestroyTextureObject(t.tex);
-    c->tex_cache.clear();
+    if (t->ptr == ptr && t->bytes >= bytes) {
+      t->users.fetch_add(1, std::memory_order_acquire);
+      t->stamp = ++c->tex_clock;
+      return TexLease(t.get(), stream);
+    }
+  if (c->tex_cache.size() >= 64) {
+    // users only grows under tex_mu, so an idle entry seen here stays idle
+    size_t victim = c->tex_cache.size();
+    for (size_t i = 0; i < c->tex_cache.size(); i++)
+      if (c->tex_cache[i]->users.load(std::memory_order_acquire) == 0 &&
+          (victim == c->tex_cache.size() || c->tex_cache[i]->stamp < c->tex_cache[victim]->stamp))
+        victim = i;
+    if (victim == c->tex_cache.size()) return {};
+    auto& v = c->tex_cache[victim];
+    if (cudaEventSynchronize(v->last) != cudaSuccess) {
+      cudaGetLastError();
+      return {};
+    }
+    cudaDestroyTextureObject(v->tex);
+    cudaEventDestroy(v->last);
+    c->tex_cache.erase(c->tex_cache.begin() + victim);
+  }
+  auto e = std::make_unique<DevCtx::Tex>();
+  if (cudaEventCreateWithFlags(&e->last, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return {};
   }
   cudaResourceDesc rd = {};
   rd.resType = cudaResourceTypeLinear;
@@ -313,22 +370,25 @@ cudaTextureObject_t tex_for(DevCtx* c, const void* ptr, size_t bytes) {
   rd.res.linear.sizeInBytes = bytes / 16 * 16;
   cudaTextureDesc td = {};
   td.readMode = cudaReadModeElementType;
-  cudaTextureObject_t tex = 0;
-  if (cudaCreateTextureObject(&tex, &rd, &td, nullptr) != cudaSuccess) {
+  if (cudaCreateTextureObject(&e->tex, &rd, &td, nullptr) != cudaSuccess) {
     cudaGetLastError();
-    return 0;
+    cudaEventDestroy(e->last);
+    return {};
   }
-  c->tex_cache.push_back({ptr, bytes, tex});
-  return tex;
+  e->ptr = ptr;
+  e->bytes = bytes;
+  e->stamp = ++c->tex_clock;
+  e->users.store(1, std::memory_order_relaxed);
+  c->tex_cache.push_back(std::move(e));
+  return TexLease(c->tex_cache.back().get(), stream);
 }
 
 // Largest launch (in 16-byte blocks) that a texture can cover on this
 // device; device-API calls above it are cut into segments so every segment
 // keeps the texture-path loads.  0 = textures unavailable.
 size_t tex_segment_blocks(DevCtx* c) {
-  tex_for(c, nullptr, 0);  // no-op; attributes are queried below on first use
   std::lock_guard<std::mutex> lk(c->tex_mu);
-  if (c->tex_align == 0) return 0;  // not queried yet: caller falls back to one launch
+  query_tex_limits(c);
   if (c->tex_align < 0) return 0;
   size_t seg = std::min<size_t>(c->tex_max_texels, 0x7FFFFFFFull);
   return seg & ~((size_t)(1 << 20) - 1);
@@ -448,11 +508,11 @@ int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t r0, size_t rows, const
     case Mode::kFolded:
       if (j.dec) {
         GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,
-                              c->sms, s.stream, tex_for(c, s.d_in, s.cap)));
+                              c->sms, s.stream, tex_for(c, s.d_in, s.cap, s.stream)));
         note_kernel("k_blocks_dec_folded");
       } else if (j.standard || g_variant.load() < 2) {
         GAES_CK(launch_enc_folded(c, s.d_in, s.d_out, nblk, compact, j.rk, ilp_default(), s.stream,
-                                  tex_for(c, s.d_in, s.cap)));
+                                  tex_for(c, s.d_in, s.cap, s.stream)));
       } else {  // bitsliced kernel has the standard S-box built in; caller tables -> T-table
         GAES_CK(launch_blocks(false, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,
                               c->sms, s.stream));
@@ -461,19 +521,19 @@ int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t r0, size_t rows, const
       break;
     case Mode::kChain:
       GAES_CK(launch_blocks(j.dec, kIvChain, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk,
-                            j.ivs ? s.d_iv : nullptr, bpr, c->sms, s.stream, tex_for(c, s.d_in, s.cap)));
+                            j.ivs ? s.d_iv : nullptr, bpr, c->sms, s.stream, tex_for(c, s.d_in, s.cap, s.stream)));
       note_kernel(j.dec ? "k_blocks_dec_chain" : "k_blocks_enc_chain");
       break;
     case Mode::kEncRows:
       GAES_CK(launch_cbc_enc_rows(s.d_in, s.d_out, rows, bpr, compact, j.rk, j.ivs ? s.d_iv : nullptr, c->sms,
-                                  s.stream, tex_for(c, s.d_in, s.cap)));
+                                  s.stream, tex_for(c, s.d_in, s.cap, s.stream)));
       note_kernel("k_cbc_enc_rows");
       break;
     case Mode::kManyKey: {
       const size_t kb = j.n_keys * 16, rkb = j.n_keys * 176;
       GAES_CK(launch_many_key(j.dec, s.d_in, s.d_out, nblk, j.first + r0, j.bpk, compact,
                               c->d_mk + kb + (j.dec ? rkb : 0), j.mk_ivs ? c->d_mk + kb + 2 * rkb : nullptr, c->sms,
-                              s.stream, tex_for(c, s.d_in, s.cap)));
+                              s.stream, tex_for(c, s.d_in, s.cap, s.stream)));
       note_kernel(j.dec ? "k_many_key_dec" : "k_many_key_enc");
       break;
     }
@@ -981,7 +1041,7 @@ GAES_API int gaes_encrypt_blocks_dev(const void* in, void* out, size_t n_blocks,
   return for_segments(c, n_blocks, [&](size_t off, size_t cnt) {
     const uint4* i = static_cast<const uint4*>(in) + off;
     GAES_CK(launch_enc_folded(c, i, static_cast<uint4*>(out) + off, cnt, c->d_std_enc, k, ilp_default(),
-                              (cudaStream_t)stream, tex_for(c, i, cnt * 16)));
+                              (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream)));
     return GAES_OK;
   });
 }
@@ -997,7 +1057,7 @@ GAES_API int gaes_decrypt_blocks_dev(const void* in, void* out, size_t n_blocks,
   return for_segments(c, n_blocks, [&](size_t off, size_t cnt) {
     const uint4* i = static_cast<const uint4*>(in) + off;
     GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), i, static_cast<uint4*>(out) + off, cnt, c->d_std_dec, k,
-                          nullptr, 1, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16)));
+                          nullptr, 1, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream)));
     note_kernel("k_blocks_dec_folded");
     return GAES_OK;
   });
@@ -1016,7 +1076,7 @@ GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m,
   const RoundKeys k = make_enc_keys(round_keys, iv, false);
   if (bpr == 1) {
     GAES_CK(launch_blocks(false, kIvChain, ilp_default(), in, out, n, c->d_std_enc, k, ivs_dev, 1, c->sms,
-                          (cudaStream_t)stream, tex_for(c, in, n * 16)));
+                          (cudaStream_t)stream, tex_for(c, in, n * 16, (cudaStream_t)stream)));
     note_kernel("k_blocks_enc_chain");
   } else {
     // segments of whole rows, each inside one texture
@@ -1028,7 +1088,7 @@ GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m,
     for (size_t r = 0; r < n; r += seg_rows) {
       const size_t cnt = std::min(seg_rows, n - r);
       GAES_CK(launch_cbc_enc_rows(i8 + r * m, o8 + r * m, cnt, bpr, c->d_std_enc, k, v8 ? v8 + r * 16 : nullptr,
-                                  c->sms, (cudaStream_t)stream, tex_for(c, i8 + r * m, cnt * m)));
+                                  c->sms, (cudaStream_t)stream, tex_for(c, i8 + r * m, cnt * m, (cudaStream_t)stream)));
     }
     note_kernel("k_cbc_enc_rows");
   }
@@ -1047,7 +1107,7 @@ GAES_API int gaes_cbc_decrypt_dev(const void* in, void* out, size_t n, size_t m,
   if (bpr == 1 && !ivs_dev) return gaes_decrypt_blocks_dev(in, out, n, round_keys, iv, stream);
   const RoundKeys k = make_dec_keys(round_keys, iv, false, nullptr);
   GAES_CK(launch_blocks(true, kIvChain, ilp_default(), in, out, n * bpr, c->d_std_dec, k, ivs_dev, bpr, c->sms,
-                        (cudaStream_t)stream, tex_for(c, in, n * bpr * 16)));
+                        (cudaStream_t)stream, tex_for(c, in, n * bpr * 16, (cudaStream_t)stream)));
   note_kernel("k_blocks_dec_chain");
   return GAES_OK;
 }
@@ -1074,7 +1134,7 @@ GAES_API int gaes_many_key_encrypt_dev(const void* in, void* out, size_t blocks_
   return for_segments(c, blocks_per_key * k, [&](size_t off, size_t cnt) {
     const uint4* i = static_cast<const uint4*>(in) + off;
     GAES_CK(launch_many_key(false, i, static_cast<uint4*>(out) + off, cnt, off, blocks_per_key, c->d_std_enc, rk_enc,
-                            ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16)));
+                            ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream)));
     note_kernel("k_many_key_enc");
     return GAES_OK;
   });
@@ -1090,7 +1150,7 @@ GAES_API int gaes_many_key_decrypt_dev(const void* in, void* out, size_t blocks_
   return for_segments(c, blocks_per_key * k, [&](size_t off, size_t cnt) {
     const uint4* i = static_cast<const uint4*>(in) + off;
     GAES_CK(launch_many_key(true, i, static_cast<uint4*>(out) + off, cnt, off, blocks_per_key, c->d_std_dec, rk_dec,
-                            ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16)));
+                            ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream)));
     note_kernel("k_many_key_dec");
     return GAES_OK;
   });

@@ -689,3 +689,36 @@ def test_host_many_key_matches_oracle(oracle, k, bpk):
     assert np.array_equal(backend_cuda.many_key_decrypt(c, keys, ivs), p)
     c0 = backend_cuda.many_key_encrypt(p, keys)  # zero IVs
     assert np.array_equal(c0[:bpk], oracle.encrypt(keys[0].tobytes(), np.zeros((bpk, 16), np.uint8), p[:bpk]))
+
+
+def test_texture_cache_churn_across_threads(oracle):
+    """Device-API calls on > 64 distinct input buffers from 4 threads: the
+    per-device texture cache evicts least-recently-used idle entries only
+    after the launches that read them (their last-use events) -- every result
+    must stay bit-exact, including buffers re-used after eviction."""
+    rng = np.random.default_rng(44)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    rk = oracle.gen_keys(key)
+    n = 4099
+    pool = [torch.from_numpy(rng.integers(0, 256, (n + i, 16), dtype=np.uint8)).cuda() for i in range(90)]
+    ref = [device.encrypt_blocks(x, rk, iv) for x in pool[:3]]
+    errors = []
+
+    def work(t):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for rep in range(3):
+                for i in range(t, len(pool), 4):
+                    x = pool[i]
+                    c = device.encrypt_blocks(x, rk, iv)
+                    d = device.decrypt_blocks(c, rk, iv)
+                    s.synchronize()
+                    if not torch.equal(d, x) or (i < 3 and not torch.equal(c, ref[i])):
+                        errors.append((t, rep, i))
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    assert not errors, errors[:5]
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (n, 1))
+    assert np.array_equal(ref[0].cpu().numpy(), oracle.encrypt(key, ivrows, pool[0].cpu().numpy()))
