@@ -394,6 +394,33 @@ size_t tex_segment_blocks(DevCtx* c) {
   return seg & ~((size_t)(1 << 20) - 1);
 }
 
+// Device-API aliasing.  Every kernel reads a block before writing the same
+// block, so out == in is safe -- except block-parallel CBC decrypt, where the
+// first lane of each warp reads its chain value in[b-1] from a block another
+// warp may already have overwritten.  Partially overlapping ranges are unsafe
+// for every kernel.  In those cases the input is first copied to a
+// stream-ordered private buffer (freed on the same stream after the launch).
+struct PrivateInput {
+  void* ptr = nullptr;
+  cudaStream_t stream = nullptr;
+  ~PrivateInput() {
+    if (ptr) cudaFreeAsync(ptr, stream);
+  }
+};
+
+int private_input_if_aliased(const void* in, const void* out, size_t bytes, bool identical_is_unsafe,
+                             cudaStream_t stream, const void** src, PrivateInput* tmp) {
+  *src = in;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(in), b = reinterpret_cast<uintptr_t>(out);
+  const bool overlap = a < b + bytes && b < a + bytes;
+  if (!overlap || (a == b && !identical_is_unsafe)) return GAES_OK;
+  GAES_CK(cudaMallocAsync(&tmp->ptr, bytes, stream));
+  tmp->stream = stream;
+  GAES_CK(cudaMemcpyAsync(tmp->ptr, in, bytes, cudaMemcpyDeviceToDevice, stream));
+  *src = tmp->ptr;
+  return GAES_OK;
+}
+
 // Runs fn(offset, count) over [0, n) in texture-sized segments.
 template <typename F>
 int for_segments(DevCtx* c, size_t n, F&& fn) {
@@ -1038,8 +1065,12 @@ GAES_API int gaes_encrypt_blocks_dev(const void* in, void* out, size_t n_blocks,
   int rc = current_ctx(&c);
   if (rc) return rc;
   const RoundKeys k = make_enc_keys(round_keys, iv, true);
+  const void* src = nullptr;
+  PrivateInput tmp;
+  rc = private_input_if_aliased(in, out, n_blocks * 16, false, (cudaStream_t)stream, &src, &tmp);
+  if (rc) return rc;
   return for_segments(c, n_blocks, [&](size_t off, size_t cnt) {
-    const uint4* i = static_cast<const uint4*>(in) + off;
+    const uint4* i = static_cast<const uint4*>(src) + off;
     GAES_CK(launch_enc_folded(c, i, static_cast<uint4*>(out) + off, cnt, c->d_std_enc, k, ilp_default(),
                               (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream)));
     return GAES_OK;
@@ -1054,8 +1085,12 @@ GAES_API int gaes_decrypt_blocks_dev(const void* in, void* out, size_t n_blocks,
   int rc = current_ctx(&c);
   if (rc) return rc;
   const RoundKeys k = make_dec_keys(round_keys, iv, true, nullptr);
+  const void* src = nullptr;
+  PrivateInput tmp;
+  rc = private_input_if_aliased(in, out, n_blocks * 16, false, (cudaStream_t)stream, &src, &tmp);
+  if (rc) return rc;
   return for_segments(c, n_blocks, [&](size_t off, size_t cnt) {
-    const uint4* i = static_cast<const uint4*>(in) + off;
+    const uint4* i = static_cast<const uint4*>(src) + off;
     GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), i, static_cast<uint4*>(out) + off, cnt, c->d_std_dec, k,
                           nullptr, 1, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream)));
     note_kernel("k_blocks_dec_folded");
@@ -1074,15 +1109,19 @@ GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m,
   const uint64_t bpr = m / 16;
   if (bpr == 1 && !ivs_dev) return gaes_encrypt_blocks_dev(in, out, n, round_keys, iv, stream);
   const RoundKeys k = make_enc_keys(round_keys, iv, false);
+  const void* src = nullptr;
+  PrivateInput tmp;
+  rc = private_input_if_aliased(in, out, n * m, false, (cudaStream_t)stream, &src, &tmp);
+  if (rc) return rc;
   if (bpr == 1) {
-    GAES_CK(launch_blocks(false, kIvChain, ilp_default(), in, out, n, c->d_std_enc, k, ivs_dev, 1, c->sms,
-                          (cudaStream_t)stream, tex_for(c, in, n * 16, (cudaStream_t)stream)));
+    GAES_CK(launch_blocks(false, kIvChain, ilp_default(), src, out, n, c->d_std_enc, k, ivs_dev, 1, c->sms,
+                          (cudaStream_t)stream, tex_for(c, src, n * 16, (cudaStream_t)stream)));
     note_kernel("k_blocks_enc_chain");
   } else {
     // segments of whole rows, each inside one texture
     const size_t seg_blocks = tex_segment_blocks(c);
     const size_t seg_rows = seg_blocks >= bpr ? seg_blocks / bpr : n;
-    const uint8_t* i8 = static_cast<const uint8_t*>(in);
+    const uint8_t* i8 = static_cast<const uint8_t*>(src);
     uint8_t* o8 = static_cast<uint8_t*>(out);
     const uint8_t* v8 = static_cast<const uint8_t*>(ivs_dev);
     for (size_t r = 0; r < n; r += seg_rows) {
@@ -1106,8 +1145,12 @@ GAES_API int gaes_cbc_decrypt_dev(const void* in, void* out, size_t n, size_t m,
   const uint64_t bpr = m / 16;
   if (bpr == 1 && !ivs_dev) return gaes_decrypt_blocks_dev(in, out, n, round_keys, iv, stream);
   const RoundKeys k = make_dec_keys(round_keys, iv, false, nullptr);
-  GAES_CK(launch_blocks(true, kIvChain, ilp_default(), in, out, n * bpr, c->d_std_dec, k, ivs_dev, bpr, c->sms,
-                        (cudaStream_t)stream, tex_for(c, in, n * bpr * 16, (cudaStream_t)stream)));
+  const void* src = nullptr;
+  PrivateInput tmp;
+  rc = private_input_if_aliased(in, out, n * m, bpr > 1, (cudaStream_t)stream, &src, &tmp);
+  if (rc) return rc;
+  GAES_CK(launch_blocks(true, kIvChain, ilp_default(), src, out, n * bpr, c->d_std_dec, k, ivs_dev, bpr, c->sms,
+                        (cudaStream_t)stream, tex_for(c, src, n * bpr * 16, (cudaStream_t)stream)));
   note_kernel("k_blocks_dec_chain");
   return GAES_OK;
 }
@@ -1131,8 +1174,12 @@ GAES_API int gaes_many_key_encrypt_dev(const void* in, void* out, size_t blocks_
   DevCtx* c = nullptr;
   int rc = current_ctx(&c);
   if (rc) return rc;
+  const void* src = nullptr;
+  PrivateInput tmp;
+  rc = private_input_if_aliased(in, out, blocks_per_key * k * 16, false, (cudaStream_t)stream, &src, &tmp);
+  if (rc) return rc;
   return for_segments(c, blocks_per_key * k, [&](size_t off, size_t cnt) {
-    const uint4* i = static_cast<const uint4*>(in) + off;
+    const uint4* i = static_cast<const uint4*>(src) + off;
     GAES_CK(launch_many_key(false, i, static_cast<uint4*>(out) + off, cnt, off, blocks_per_key, c->d_std_enc, rk_enc,
                             ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream)));
     note_kernel("k_many_key_enc");
@@ -1147,8 +1194,12 @@ GAES_API int gaes_many_key_decrypt_dev(const void* in, void* out, size_t blocks_
   DevCtx* c = nullptr;
   int rc = current_ctx(&c);
   if (rc) return rc;
+  const void* src = nullptr;
+  PrivateInput tmp;
+  rc = private_input_if_aliased(in, out, blocks_per_key * k * 16, false, (cudaStream_t)stream, &src, &tmp);
+  if (rc) return rc;
   return for_segments(c, blocks_per_key * k, [&](size_t off, size_t cnt) {
-    const uint4* i = static_cast<const uint4*>(in) + off;
+    const uint4* i = static_cast<const uint4*>(src) + off;
     GAES_CK(launch_many_key(true, i, static_cast<uint4*>(out) + off, cnt, off, blocks_per_key, c->d_std_dec, rk_dec,
                             ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream)));
     note_kernel("k_many_key_dec");
