@@ -139,7 +139,11 @@ GAES_API int gaes_many_key_decrypt(const uint8_t *data, size_t blocks_per_key, s
 
 /* ---- device-resident entry points (stream-ordered, current device) ----
  * Standard tables from the device GF layer.  `iv` is a 16-byte HOST
- * array (shared IV, folded into the round keys) or NULL for a zero IV. */
+ * array (shared IV, folded into the round keys) or NULL for a zero IV.
+ * `out` may equal `in` or overlap it: where a kernel would read a block
+ * another thread may already have overwritten (CBC decrypt of multi-block
+ * rows in place, any partial overlap) the input is first copied to a
+ * private stream-ordered buffer. */
 
 /* n_blocks independent 16-byte rows: out_i = E_K(in_i ^ iv)   (M = 16). */
 GAES_API int gaes_encrypt_blocks_dev(const void *in, void *out, size_t n_blocks,
