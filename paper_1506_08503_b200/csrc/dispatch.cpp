@@ -487,6 +487,22 @@ bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// Device address of a pinned (page-locked, mapped) host pointer, or nullptr.
+const uint8_t* host_dev_view(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? static_cast<const uint8_t*>(a.devicePointer) : nullptr;
+}
+
+// Jobs up to this size on pinned caller buffers run as one zero-copy launch.
+size_t zero_copy_bytes() {
+  static size_t b = (size_t)std::max(0, env_int("GAES_ZEROCOPY_MB", 64)) << 20;
+  return b;
+}
+
 size_t chunk_bytes() {
   static size_t b = (size_t)std::max(1, env_int("GAES_CHUNK_MB", 32)) << 20;
   return b;
@@ -528,46 +544,50 @@ int finish_slot(Slot& s) {
   return GAES_OK;
 }
 
-int launch_chunk(DevCtx* c, const Job& j, Slot& s, size_t r0, size_t rows, const uint32_t* compact) {
+// One kernel launch over rows [r0, r0 + rows) of job j: `in` / `out` / `ivs`
+// hold exactly those rows (device staging buffers, or the caller's pinned
+// host buffers for a zero-copy launch); `tin` is a texture over `in` or 0.
+int launch_chunk(DevCtx* c, const Job& j, cudaStream_t stream, const uint8_t* in, uint8_t* out,
+                 const uint8_t* ivs, size_t r0, size_t rows, const uint32_t* compact, cudaTextureObject_t tin) {
   const uint64_t bpr = j.m / 16;
   const uint64_t nblk = rows * bpr;
   switch (j.mode) {
     case Mode::kFolded:
       if (j.dec) {
-        GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,
-                              c->sms, s.stream, tex_for(c, s.d_in, s.cap, s.stream)));
+        GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), in, out, nblk, compact, j.rk, nullptr, 1,
+                              c->sms, stream, tin));
         note_kernel("k_blocks_dec_folded");
       } else if (j.standard || g_variant.load() < 2) {
-        GAES_CK(launch_enc_folded(c, s.d_in, s.d_out, nblk, compact, j.rk, ilp_default(), s.stream,
-                                  tex_for(c, s.d_in, s.cap, s.stream)));
+        GAES_CK(launch_enc_folded(c, in, out, nblk, compact, j.rk, ilp_default(), stream,
+                                  tin));
       } else {  // bitsliced kernel has the standard S-box built in; caller tables -> T-table
-        GAES_CK(launch_blocks(false, kIvFolded, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk, nullptr, 1,
-                              c->sms, s.stream));
+        GAES_CK(launch_blocks(false, kIvFolded, ilp_default(), in, out, nblk, compact, j.rk, nullptr, 1,
+                              c->sms, stream));
         note_kernel("k_blocks_enc_folded");
       }
       break;
     case Mode::kChain:
-      GAES_CK(launch_blocks(j.dec, kIvChain, ilp_default(), s.d_in, s.d_out, nblk, compact, j.rk,
-                            j.ivs ? s.d_iv : nullptr, bpr, c->sms, s.stream, tex_for(c, s.d_in, s.cap, s.stream)));
+      GAES_CK(launch_blocks(j.dec, kIvChain, ilp_default(), in, out, nblk, compact, j.rk,
+                            j.ivs ? ivs : nullptr, bpr, c->sms, stream, tin));
       note_kernel(j.dec ? "k_blocks_dec_chain" : "k_blocks_enc_chain");
       break;
     case Mode::kEncRows:
-      GAES_CK(launch_cbc_enc_rows(s.d_in, s.d_out, rows, bpr, compact, j.rk, j.ivs ? s.d_iv : nullptr, c->sms,
-                                  s.stream, tex_for(c, s.d_in, s.cap, s.stream)));
+      GAES_CK(launch_cbc_enc_rows(in, out, rows, bpr, compact, j.rk, j.ivs ? ivs : nullptr, c->sms,
+                                  stream, tin));
       note_kernel("k_cbc_enc_rows");
       break;
     case Mode::kManyKey: {
       const size_t kb = j.n_keys * 16, rkb = j.n_keys * 176;
-      GAES_CK(launch_many_key(j.dec, s.d_in, s.d_out, nblk, j.first + r0, j.bpk, compact,
+      GAES_CK(launch_many_key(j.dec, in, out, nblk, j.first + r0, j.bpk, compact,
                               c->d_mk + kb + (j.dec ? rkb : 0), j.mk_ivs ? c->d_mk + kb + 2 * rkb : nullptr, c->sms,
-                              s.stream, tex_for(c, s.d_in, s.cap, s.stream)));
+                              stream, tin));
       note_kernel(j.dec ? "k_many_key_dec" : "k_many_key_enc");
       break;
     }
     case Mode::kGeneric: {
       uint8_t* sc = c->d_scratch;
-      GAES_CK(launch_generic(j.dec, s.d_in, s.d_iv, rows, j.m, sc + 256 + 4096 + 16, sc, sc + 256, sc + 256 + 4096,
-                             s.d_out, c->sms, s.stream));
+      GAES_CK(launch_generic(j.dec, in, ivs, rows, j.m, sc + 256 + 4096 + 16, sc, sc + 256, sc + 256 + 4096,
+                             out, c->sms, stream));
       note_kernel("k_generic_cbc");
       break;
     }
@@ -641,14 +661,41 @@ int run_job(DevCtx* c, const Job& j) {
 
   const bool in_pinned = is_pinned(j.data);
   const bool out_pinned = is_pinned(j.out);
+  if (!(in_pinned && out_pinned) && j.n * j.m >= ((size_t)256 << 10)) host_pool().warm();
   const bool need_iv = j.ivs != nullptr;
   const bool iv_pinned = need_iv && is_pinned(j.ivs);
+
+  // Pinned caller buffers and a job small enough that the staged pipeline's
+  // ramp dominates: one zero-copy launch -- the kernel reads and writes the
+  // caller's host memory over PCIe itself, no staging copies
+  // (scripts/exp/zerocopy_probe.py: 21 vs 15 GB/s at 1 MiB, 34 vs 32 at
+  // 16 MiB, 38.6 vs 37.9 at 64 MiB; the staged pipeline leads from 256 MiB).
+  // Not for byte-level generic tables (byte loads over PCIe) nor for
+  // overlapping in/out (the kernels assume distinct buffers).
+  const size_t total = j.n * j.m;
+  const uintptr_t ia = reinterpret_cast<uintptr_t>(j.data), oa = reinterpret_cast<uintptr_t>(j.out);
+  if (in_pinned && out_pinned && (!need_iv || iv_pinned) && j.mode != Mode::kGeneric && total <= zero_copy_bytes() &&
+      !(ia < oa + total && oa < ia + total)) {
+    const uint8_t* din = host_dev_view(j.data);
+    uint8_t* dout = const_cast<uint8_t*>(host_dev_view(j.out));
+    const uint8_t* div = need_iv ? host_dev_view(j.ivs) : nullptr;
+    if (din && dout && (!need_iv || div)) {
+      cudaStream_t st = c->slots[0].stream;
+      int rc = launch_chunk(c, j, st, din, dout, div, 0, j.n, compact, 0);
+      if (rc) return rc;
+      GAES_CK(cudaStreamSynchronize(st));
+      drain.armed = false;
+      return GAES_OK;
+    }
+  }
   // Chunk schedule: ramp up from base/8 so the first H2D is short (nothing
   // overlaps it), run at `base`, ramp down at the end so the last D2H is
   // short too.  All chunks are whole rows.
   // Pageable buffers are staged by host copies: smaller chunks let the copy
   // of chunk c+1 overlap the DMA of chunk c.
-  const size_t base_bytes = (in_pinned && out_pinned) ? chunk_bytes() : std::min<size_t>(chunk_bytes(), 8u << 20);
+  // pageable callers: 16 MiB (17.0 vs 16.3 / 15.2 GB/s with 8 / 4 MiB, 16 threads)
+  static const size_t pageable_chunk = (size_t)std::max(1, env_int("GAES_PAGEABLE_CHUNK_MB", 16)) << 20;
+  const size_t base_bytes = (in_pinned && out_pinned) ? chunk_bytes() : std::min<size_t>(chunk_bytes(), pageable_chunk);
   const size_t base_rows = std::max<size_t>(1, base_bytes / j.m);
   const size_t min_rows = std::max<size_t>(1, base_rows / 8);
   std::vector<std::pair<size_t, size_t>> chunks;  // (first row, rows)
@@ -696,7 +743,8 @@ int run_job(DevCtx* c, const Job& j) {
       }
       GAES_CK(cudaMemcpyAsync(s.d_iv, ivsrc, rows * 16, cudaMemcpyHostToDevice, s.stream));
     }
-    int rc = launch_chunk(c, j, s, r0, rows, compact);
+    int rc = launch_chunk(c, j, s.stream, s.d_in, s.d_out, s.d_iv, r0, rows, compact,
+                          tex_for(c, s.d_in, s.cap, s.stream));
     if (rc) return rc;
     if (out_pinned) {
       GAES_CK(cudaMemcpyAsync(j.out + off, s.d_out, bytes, cudaMemcpyDeviceToHost, s.stream));
@@ -778,7 +826,7 @@ int run_sharded(const Job& j) {
 // the IV folds into the key and the grid never crosses PCIe.
 bool rows_share_iv(const uint8_t* ivs, size_t n) {
   std::atomic<bool> same{true};
-  parallel_ranges(n, (size_t)1 << 18, [&](size_t lo, size_t hi) {
+  parallel_ranges(n, (size_t)1 << 13, [&](size_t lo, size_t hi) {
     uint64_t a0, a1;
     std::memcpy(&a0, ivs, 8);
     std::memcpy(&a1, ivs + 8, 8);
@@ -834,6 +882,7 @@ int cbc_host(bool dec, const uint8_t* data, const uint8_t* ivs, size_t n, size_t
     return run_sharded(j);
   }
   const size_t bpr = m / 16;
+  if (n >= ((size_t)1 << 14)) host_pool().warm();  // parallel IV scan + staging copies follow
   const bool shared = rows_share_iv(ivs, n);
   if (bpr == 1 && shared) {
     j.mode = Mode::kFolded;

@@ -2,8 +2,11 @@
 // (pageable <-> pinned copies, shared-IV detection).  Internal to
 // libgaes_b200.so.
 #pragma once
+#include <sched.h>
+
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
@@ -21,17 +24,36 @@ namespace host {
 // pageable buffers are copied by several threads: one core's memcpy (~10 GB/s)
 // is slower than a PCIe Gen5 DMA, so a single-threaded staging copy would
 // bound the drop-in path.
+// Default: every CPU this process may run on (its affinity mask -- one
+// NUMA node per rank under bench.py's binding), at most 32.  Measured on the
+// 16-CPU GPU box (scripts/exp/dropin_probe.py, 64 MiB pageable drop-in):
+// 11.9 / 14.6 / 16.3 GB/s with 8 / 12 / 16 threads.
 inline int host_threads() {
   static int t = [] {
-    int hw = (int)std::thread::hardware_concurrency();
+    int cpus = (int)std::thread::hardware_concurrency();
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) cpus = CPU_COUNT(&set);
     const char* e = std::getenv("GAES_HOST_THREADS");
-    int v = (e && *e) ? std::atoi(e) : std::max(1, std::min(12, hw - 4));
+    int v = (e && *e) ? std::atoi(e) : std::min(32, cpus);
     return std::max(1, v);
   }();
   return t;
 }
 
-// Persistent workers (spawning threads per staging copy costs ~50 us).
+inline void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+  __builtin_ia32_pause();
+#else
+  std::this_thread::yield();
+#endif
+}
+
+// Persistent workers (spawning threads per staging copy costs ~50 us).  A
+// worker woken from a condition-variable sleep can take a few hundred
+// microseconds to run on the GPU box (scripts/exp/dropin_probe.py: 1 MiB
+// drop-in calls were slower with the pool than on one thread), so after each
+// region workers spin for a short window before sleeping, and warm() lets a
+// caller wake them ahead of a burst of regions (a staged pipeline).
 class HostPool {
  public:
   explicit HostPool(int n) {
@@ -40,7 +62,7 @@ class HostPool {
   ~HostPool() {
     {
       std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
+      stop_.store(true);
     }
     cv_.notify_all();
     for (auto& w : workers_) w.join();
@@ -54,7 +76,7 @@ class HostPool {
       parts_ = parts;
       next_.store(0);
       pending_ = parts;
-      gen_++;
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     work();
@@ -62,8 +84,18 @@ class HostPool {
     done_cv_.wait(lk, [this] { return pending_ == 0; });
     fn_ = nullptr;
   }
+  // Wakes sleeping workers into their spin window (no work).
+  void warm() {
+    if (workers_.empty()) return;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      wake_++;
+    }
+    cv_.notify_all();
+  }
 
  private:
+  static constexpr auto kSpin = std::chrono::microseconds(400);
   void work() {
     for (;;) {
       const size_t i = next_.fetch_add(1);
@@ -74,13 +106,25 @@ class HostPool {
     }
   }
   void loop() {
-    uint64_t seen = 0;
+    uint64_t seen = 0, seen_wake = 0;
     for (;;) {
+      const auto t0 = std::chrono::steady_clock::now();
+      for (int k = 0; gen_.load(std::memory_order_acquire) == seen && !stop_.load(); k++) {
+        if ((k & 63) == 0 && std::chrono::steady_clock::now() - t0 > kSpin) break;
+        cpu_relax();
+      }
       {
         std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return stop_ || (gen_ != seen && fn_ != nullptr); });
-        if (stop_) return;
-        seen = gen_;
+        cv_.wait(lk, [&] {
+          return stop_.load() || (gen_.load() != seen && fn_ != nullptr) || wake_ != seen_wake;
+        });
+        if (stop_.load()) return;
+        seen_wake = wake_;
+        if (!(gen_.load() != seen && fn_ != nullptr)) {  // warm-up only: spin for the next region
+          seen = gen_.load();
+          continue;
+        }
+        seen = gen_.load();
       }
       work();
     }
@@ -91,8 +135,9 @@ class HostPool {
   const std::function<void(size_t)>* fn_ = nullptr;
   size_t parts_ = 0, pending_ = 0;
   std::atomic<size_t> next_{0};
-  uint64_t gen_ = 0;
-  bool stop_ = false;
+  std::atomic<uint64_t> gen_{0};
+  uint64_t wake_ = 0;
+  std::atomic<bool> stop_{false};
 };
 
 inline HostPool& host_pool() {
@@ -116,7 +161,11 @@ void parallel_ranges(size_t n, size_t min_per_thread, F&& fn) {
 }
 
 inline void par_memcpy(void* dst, const void* src, size_t bytes) {
-  parallel_ranges(bytes, (size_t)512 << 10, [&](size_t lo, size_t hi) {
+  static const size_t grain = [] {
+    const char* e = std::getenv("GAES_MEMCPY_GRAIN_KB");
+    return (size_t)std::max(16, (e && *e) ? std::atoi(e) : 128) << 10;
+  }();
+  parallel_ranges(bytes, grain, [&](size_t lo, size_t hi) {
     std::memcpy((uint8_t*)dst + lo, (const uint8_t*)src + lo, hi - lo);
   });
 }

@@ -768,3 +768,51 @@ def test_device_api_in_place_and_overlapping(oracle, shift):
         assert torch.equal(got, want), i
     want = oracle.decrypt(key, ivs.cpu().numpy(), p.cpu().numpy())
     assert np.array_equal(aliased(p, lambda a, o: device.cbc_decrypt(a, rk, ivs, out=o)).cpu().numpy(), want)
+
+
+def _pinned(shape, rng=None):
+    t = torch.empty(shape, dtype=torch.uint8).pin_memory()
+    a = t.numpy()
+    if rng is not None:
+        a[:] = rng.integers(0, 256, shape, dtype=np.uint8)
+    return t, a
+
+
+@pytest.mark.parametrize("n,m", [(1, 16), (4097, 16), (4096, 16), (3001, 64), (1 << 20, 16)])
+def test_pinned_zero_copy_every_mode(oracle, n, m):
+    """Pinned host buffers up to GAES_ZEROCOPY_MB run as one zero-copy launch
+    (the kernel reads and writes host memory over PCIe); every host entry
+    point must match the oracle there, with pinned per-row IVs too, and
+    in-place pinned calls (which take the staged pipeline) as well."""
+    rng = np.random.default_rng(n + m)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    rk = oracle.gen_keys(key)
+    _t0, p = _pinned((n, m), rng)
+    _t1, ivs = _pinned((n, 16), rng)
+    _t2, out = _pinned((n, m))
+    _t3, back = _pinned((n, m))
+    tables = oracle.encrypt_tables(key)
+    want = oracle.encrypt(key, ivs, p, threads=4)
+    backend_cuda.cbc_encrypt(p, ivs, *tables, out)                     # per-row IVs (chain / rows)
+    assert np.array_equal(out, want)
+    backend_cuda.cbc_decrypt(out, ivs, *oracle.decrypt_tables(key), back)
+    assert np.array_equal(back, p)
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (n, 1))
+    want = oracle.encrypt(key, ivrows, p, threads=4)
+    backend_cuda.encrypt_shared_iv(p, iv, rk, out=out)                  # folded / rows, shared IV
+    assert np.array_equal(out, want)
+    backend_cuda.decrypt_shared_iv(out, iv, rk, out=back)
+    assert np.array_equal(back, p)
+    backend_cuda.encrypt_shared_iv(back, iv, rk, out=back)              # in place (staged path)
+    assert np.array_equal(back, want)
+    if m == 16 and n % 16 == 0:
+        k = 16
+        keys = rng.integers(0, 256, (k, 16), dtype=np.uint8)
+        kivs = rng.integers(0, 256, (k, 16), dtype=np.uint8)
+        backend_cuda.many_key_encrypt(p, keys, kivs, out=out)
+        bpk = n // k
+        for i in (0, k - 1):
+            r = slice(i * bpk, (i + 1) * bpk)
+            assert np.array_equal(out[r], oracle.encrypt(keys[i].tobytes(), np.tile(kivs[i], (bpk, 1)), p[r]))
+        backend_cuda.many_key_decrypt(out, keys, kivs, out=back)
+        assert np.array_equal(back, p)
