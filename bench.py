@@ -282,9 +282,20 @@ def cpu_baseline(key, iv, budget_s: float):
     n = int(min(1 << 26, max(probe_n, rate * budget_s / 2)))
     times, kind = cpu_reference_rate(key, iv, n, threads, reps=4, warm=0)
     sec = statistics.median(times)
+    # W = 1 beside W = all: the reference kernel on one thread
+    n1 = 1 << 20
+    t1, _ = cpu_reference_rate(key, iv, n1, 1, reps=1, warm=0)
+    try:
+        import psutil
+        physical = psutil.cpu_count(logical=False)
+    except Exception:  # pragma: no cover
+        physical = None
     return {"value": n * BYTES_PER_BLOCK / sec / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
             "sample": f"{n} uniform 16-B blocks (shared IV, seed {SEED + 1}), median of 4 reps, "
-                      f"{threads} threads over parallel.plan chunks"}
+                      f"{threads} threads over parallel.plan chunks",
+            "single_thread": {"value": round(n1 * BYTES_PER_BLOCK / t1[0] / 1e9, 4), "unit": "GB/s",
+                              "sample": f"{n1} blocks, 1 thread"},
+            "logical_cpus": threads, "physical_cores": physical}
 
 
 def _openssl_worker(args):
