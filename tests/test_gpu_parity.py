@@ -562,6 +562,15 @@ for n, m in [(1, 16), (3, 16), (100001, 16), (5003, 48)]:
         assert np.array_equal(back, data), (n, m, g)
         ct = backend_cuda.encrypt_shared_iv(data, iv, rk)
         assert np.array_equal(backend_cuda.decrypt_shared_iv(ct, iv, rk), data)
+import torch
+for n in (5, 300001):  # pinned buffers: one zero-copy launch per shard
+    hp = torch.from_numpy(rng.integers(0, 256, (n, 16), dtype=np.uint8)).pin_memory()
+    ho = torch.empty_like(hp).pin_memory()
+    want = oracle.encrypt(key, np.tile(np.frombuffer(iv, np.uint8), (n, 1)), hp.numpy(), threads=4)
+    for g in (1, 2):
+        _lib.set_num_gpus(g)
+        backend_cuda.encrypt_shared_iv(hp.numpy(), iv, rk, out=ho.numpy())
+        assert np.array_equal(ho.numpy(), want), (n, g)
 keys = rng.integers(0, 256, (7, 16), dtype=np.uint8)
 kivs = rng.integers(0, 256, (7, 16), dtype=np.uint8)
 p = rng.integers(0, 256, (7 * 10001, 16), dtype=np.uint8)
