@@ -825,3 +825,51 @@ def test_pinned_zero_copy_every_mode(oracle, n, m):
             assert np.array_equal(out[r], oracle.encrypt(keys[i].tobytes(), np.tile(kivs[i], (bpk, 1)), p[r]))
         backend_cuda.many_key_decrypt(out, keys, kivs, out=back)
         assert np.array_equal(back, p)
+
+
+@pytest.mark.parametrize("n", [1, 31, 33, 1025, 148 * 1024 + 3])
+def test_no_out_of_bounds_writes(oracle, n):
+    """Guard bands around every output (device and host): no kernel or copy
+    may write outside [out, out + n*m).  compute-sanitizer is not available
+    on the GPU pool, so out-of-bounds writes are caught by canaries."""
+    G = 4096
+    rng = np.random.default_rng(n)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    rk = oracle.gen_keys(key)
+    keys = torch.from_numpy(rng.integers(0, 256, (1, 16), dtype=np.uint8)).cuda()
+    rke, rkd = device.expand_keys(keys)
+
+    def guarded_dev(shape):
+        numel = int(np.prod(shape))
+        buf = torch.full((numel + 2 * G,), 0xA5, dtype=torch.uint8, device="cuda")
+        return buf, buf[G:G + numel].view(shape)
+
+    def intact(buf, numel):
+        torch.cuda.synchronize()
+        return bool((buf[:G] == 0xA5).all()) and bool((buf[G + numel:] == 0xA5).all())
+
+    for m in (16, 48, 64):
+        p = torch.from_numpy(rng.integers(0, 256, (n, m), dtype=np.uint8)).cuda()
+        ivs = torch.from_numpy(rng.integers(0, 256, (n, 16), dtype=np.uint8)).cuda()
+        calls = [lambda o: device.cbc_encrypt(p, rk, iv, out=o), lambda o: device.cbc_encrypt(p, rk, ivs, out=o),
+                 lambda o: device.cbc_decrypt(p, rk, iv, out=o), lambda o: device.cbc_decrypt(p, rk, ivs, out=o)]
+        if m == 16:
+            calls += [lambda o: device.encrypt_blocks(p, rk, iv, out=o), lambda o: device.decrypt_blocks(p, rk, iv, out=o),
+                      lambda o: device.many_key_encrypt(p, rke, out=o), lambda o: device.many_key_decrypt(p, rkd, out=o)]
+        for i, call in enumerate(calls):
+            buf, o = guarded_dev((n, m))
+            call(o)
+            assert intact(buf, n * m), (m, i)
+        # host entry points (zero-copy for pinned, staged for pageable; generic tables)
+        ph = p.cpu().numpy()
+        ivh = ivs.cpu().numpy()
+        t = oracle.encrypt_tables(key)
+        perm = np.ascontiguousarray(np.roll(t[3], 1))
+        for pinned in (False, True):
+            for tables in (t, (t[0], t[1], t[2], perm)):
+                hb = torch.full((n * m + 2 * G,), 0xA5, dtype=torch.uint8)
+                if pinned:
+                    hb = hb.pin_memory()
+                a = hb.numpy()
+                backend_cuda.cbc_encrypt(ph, ivh, *tables, a[G:G + n * m].reshape(n, m))
+                assert (a[:G] == 0xA5).all() and (a[G + n * m:] == 0xA5).all(), (m, pinned)
