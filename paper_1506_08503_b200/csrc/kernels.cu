@@ -108,11 +108,17 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
              const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
              const uint4* __restrict__ ivs, uint64_t bpr, cudaTextureObject_t tin) {
   extern __shared__ __align__(1024) char smem[];
+  // Warp-interleaved block map: warp w of CTA c owns the 32 consecutive
+  // blocks starting at 32 (w * gridDim + c), so a batch smaller than the
+  // grid spreads over every SM instead of filling the first CTAs (and the
+  // last grid-stride pass of a large batch is shared by all SMs).  A CTA
+  // with no block at all exits before its table fill.
+  if ((uint64_t)blockIdx.x * 32 >= n_blocks) return;
   pdl_prologue(smem, compact);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lb = lane * 4;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
-  uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t b = ((uint64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x) * 32 + lane;
 
   uint4 cur[ILP];
 #pragma unroll
@@ -542,7 +548,8 @@ static cudaError_t launch_blocks_t(const void* in, void* out, uint64_t n, const 
   auto kern = k_blocks<ILP, DEC, IVM, TEXIN>;
   cudaError_t e = set_smem(kern);
   if (e != cudaSuccess) return e;
-  const int grid = grid_for(n, ILP, sms);
+  // every SM that gets at least one warp's 32 blocks (see k_blocks' map)
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(sms, (n + 31) / 32));
   return launch_pdl(kern, grid, kBlockThreads, kSmemBytes, s, (const uint4*)in, (uint4*)out, n, compact, rk,
                     (const uint4*)ivs, bpr, tin);
 }

@@ -19,6 +19,29 @@ __global__ void __launch_bounds__(256, 1) fill256_k(const uint32_t* compact, int
   fill_tables(smem, compact);
   if (threadIdx.x == 9999) sink[0] = smem[0];
 }
+// GPU-side cost per launch: 200 launches captured in a CUDA graph, replayed
+// (host enqueue rate out of the picture).
+template <typename F>
+float timeit_graph(F f) {
+  cudaStream_t s;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal);
+  for (int i = 0; i < 200; i++) f(s);
+  cudaStreamEndCapture(s, &g);
+  cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphLaunch(ge, s);
+  cudaStreamSynchronize(s);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  cudaEventRecord(a, s);
+  cudaGraphLaunch(ge, s);
+  cudaEventRecord(b, s);
+  cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  return ms / 200 * 1e3;
+}
 template <typename F>
 float timeit(F f) {
   cudaEvent_t a, b;
@@ -44,5 +67,9 @@ int main() {
   cudaFuncSetAttribute(fill256_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   printf("148 x 256 thr, 192 KiB smem, fill:    %.2f us\n", timeit([&] { fill256_k<<<148, 256, kSmemBytes>>>(tab, sink); }));
   printf("148 x 256 thr, no smem, empty:        %.2f us\n", timeit([&] { empty_k<<<148, 256, 0>>>(sink); }));
+  printf("graph: small kernel (1 CTA x 32):           %.2f us\n", timeit_graph([&](cudaStream_t s) { small_k<<<1, 32, 0, s>>>(sink); }));
+  printf("graph: 148 x 1024 thr, 192 KiB smem, empty:  %.2f us\n", timeit_graph([&](cudaStream_t s) { empty_k<<<148, 1024, kSmemBytes, s>>>(sink); }));
+  printf("graph: 148 x 1024 thr, 192 KiB smem, fill:   %.2f us\n", timeit_graph([&](cudaStream_t s) { fill_k<<<148, 1024, kSmemBytes, s>>>(tab, sink); }));
+  printf("graph: 148 x 256 thr, 192 KiB smem, fill:    %.2f us\n", timeit_graph([&](cudaStream_t s) { fill256_k<<<148, 256, kSmemBytes, s>>>(tab, sink); }));
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
 }
