@@ -649,25 +649,32 @@ def main():
                 traffic = json.load(f).get(f"cfg{args.config}")
         except (OSError, ValueError):
             traffic = None
-    probe = None
+    probe = lds_measured = None
     try:
         import ctypes
         rate, pms = ctypes.c_double(), ctypes.c_double()
         _lib.check(_lib.lib().gaes_probe_round_rate(local, 256, ctypes.addressof(rate), ctypes.addressof(pms)))
         probe = rate.value / 1e9
+        # the roofline denominator, measured on this GPU in this run: a
+        # conflict-free LDS.32 stream on every lane of every SM
+        _lib.check(_lib.lib().gaes_probe_lds_peak(local, 4096, ctypes.addressof(rate), ctypes.addressof(pms)))
+        lds_measured = rate.value / 1e9
     except Exception:  # pragma: no cover - informational only
-        probe = None
+        pass
+    peak = lds_measured or lds_peak
     roofline = {
         "bound": "smem", "kernel": "k_blocks_enc_folded" if args.config != 5 else "k_many_key_enc",
-        "achieved": round(lds_achieved, 2), "peak": round(lds_peak, 2), "unit": "Glookup/s",
-        "frac": round(lds_achieved / lds_peak, 4), "traffic": traffic,
+        "achieved": round(lds_achieved, 2), "peak": round(peak, 2), "unit": "Glookup/s",
+        "frac": round(lds_achieved / peak, 4), "traffic": traffic,
         "traffic_unit": "GB per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, profiles/traffic.json)",
         "algorithmic_gb_per_launch": round(n * HBM_BYTES_PER_BLOCK / 1e9, 4),
-        "per_block": f"{LOOKUPS_PER_BLOCK} conflict-free 4-B LDS lookups; peak = {sms} SMs x 32 lanes/clk x "
-                     f"{sm_mhz:.0f} MHz (median SM clock sampled during the timed region)",
-        "peak_source": "nominal: 32 conflict-free LDS lanes/clk/SM x SMs x sampled SM clock "
-                       "(MEASURED_PEAKS.json has no shared-memory figure); probe_round_rate = measured "
-                       "ceiling of this formulation on this GPU",
+        "per_block": f"{LOOKUPS_PER_BLOCK} conflict-free 4-B LDS lookups per 16-B block",
+        "peak_source": ("measured: gaes_probe_lds_peak (k_lds_peak, conflict-free LDS.32 stream on every lane, "
+                        f"{sms} SMs x 1024 threads) in this run; MEASURED_PEAKS.json has no shared-memory figure"
+                        if lds_measured else "nominal (probe unavailable): 32 LDS lanes/clk/SM x SMs x SM clock"),
+        "nominal_peak": round(lds_peak, 2),
+        "nominal_frac": round(lds_achieved / lds_peak, 4),
+        "nominal_note": f"{sms} SMs x 32 lanes/clk x {sm_mhz:.0f} MHz (median SM clock sampled during the timed region)",
         "probe_round_rate": round(probe, 2) if probe else None,
         "probe_frac": round(lds_achieved / probe, 4) if probe else None,
         "probe_note": "k_round_probe: same round function on register-resident states, no HBM (formulation ceiling)",

@@ -193,6 +193,11 @@ GAES_API const char *gaes_last_kernel(void);
  * report the achieved table-lookup rate (160 lookups per encryption) -- the
  * measured ceiling of the shared-memory T-table formulation. */
 GAES_API int gaes_probe_round_rate(int device, uint32_t iters, double *lookups_per_sec, double *ms);
+/* Roofline denominator: the shared-memory lookup peak measured on this GPU
+ * -- every lane of 1024-thread CTAs on all SMs streams conflict-free 4-byte
+ * LDS (lane l hits bank l, as the table lookups do), `iters` x 16 per
+ * thread; reports 4-byte lookups per second. */
+GAES_API int gaes_probe_lds_peak(int device, uint32_t iters, double *lookups_per_sec, double *ms);
 /* Select the M=16 encrypt/decrypt formulation: 0 = auto (fastest measured),
  * 1 = T-table in shared memory, 2 = bitsliced.  Returns the value set or
  * GAES_EINVAL if the variant is not built. */

@@ -52,6 +52,7 @@ SIGNATURES = {
     "gaes_last_kernel": (ctypes.c_char_p, []),
     "gaes_set_variant": (_i, [_i]),
     "gaes_probe_round_rate": (_i, [_i, ctypes.c_uint32, _vp, _vp]),
+    "gaes_probe_lds_peak": (_i, [_i, ctypes.c_uint32, _vp, _vp]),
 }
 
 

@@ -999,6 +999,41 @@ GAES_API int gaes_probe_round_rate(int device, uint32_t iters, double* lookups_p
   return GAES_OK;
 }
 
+GAES_API int gaes_probe_lds_peak(int device, uint32_t iters, double* lookups_per_sec, double* ms) {
+  DevCtx* c = nullptr;
+  int rc = get_ctx(device, &c);
+  if (rc) return rc;
+  int prev = 0;
+  GAES_CK(cudaGetDevice(&prev));
+  DeviceGuard guard(prev);
+  GAES_CK(cudaSetDevice(c->dev));
+  struct Res {
+    uint32_t* sink = nullptr;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ~Res() {
+      if (sink) cudaFree(sink);
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+    }
+  } r;
+  GAES_CK(cudaMalloc(&r.sink, 4));
+  GAES_CK(cudaEventCreate(&r.a));
+  GAES_CK(cudaEventCreate(&r.b));
+  GAES_CK(launch_lds_peak(64, r.sink, c->sms, 0));  // warm-up
+  GAES_CK(cudaEventRecord(r.a, 0));
+  GAES_CK(launch_lds_peak(iters, r.sink, c->sms, 0));
+  GAES_CK(cudaEventRecord(r.b, 0));
+  GAES_CK(cudaEventSynchronize(r.b));
+  note_kernel("k_lds_peak");
+  note_kernel("k_lds_peak");
+  float t = 0;
+  GAES_CK(cudaEventElapsedTime(&t, r.a, r.b));
+  const double lookups = (double)c->sms * kBlockThreads * (double)iters * 16.0;
+  if (lookups_per_sec) *lookups_per_sec = lookups / (t / 1e3);
+  if (ms) *ms = t;
+  return GAES_OK;
+}
+
 GAES_API int gaes_gf_tables(int device, uint8_t sbox[256], uint8_t inv_sbox[256], uint32_t te[1024],
                             uint32_t td[1024]) {
   DevCtx* c = nullptr;

@@ -483,6 +483,38 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
   if ((s0 ^ s1 ^ s2 ^ s3) == 0x12345678u) sink[0] = s0;  // keep the work alive
 }
 
+// Shared-memory lookup peak (roofline denominator, measured): every lane
+// streams conflict-free 4-byte LDS (lane l reads bank l, like the table
+// lookups) with no address arithmetic in the loop, 16 per iteration into 8
+// independent XOR chains -- the L1/shared data pipe's wavefront rate.
+template <int OFF>
+__device__ __forceinline__ uint32_t lds_peak_ld(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(OFF));
+  return v;
+}
+__global__ void __launch_bounds__(kBlockThreads, 1) k_lds_peak(uint32_t iters, uint32_t* __restrict__ sink) {
+  extern __shared__ __align__(1024) char smem[];
+  for (int i = threadIdx.x; i < kSmemBytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(i, i * 3, i * 5, i * 7);
+  __syncthreads();
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem) + (threadIdx.x & 31) * 4 +
+                        ((threadIdx.x >> 5) & 15) * 4096;
+  uint32_t a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (uint32_t it = 0; it < iters; it++) {
+    a[0] ^= lds_peak_ld<0>(base) ^ lds_peak_ld<128>(base);
+    a[1] ^= lds_peak_ld<256>(base) ^ lds_peak_ld<384>(base);
+    a[2] ^= lds_peak_ld<512>(base) ^ lds_peak_ld<640>(base);
+    a[3] ^= lds_peak_ld<768>(base) ^ lds_peak_ld<896>(base);
+    a[4] ^= lds_peak_ld<1024>(base) ^ lds_peak_ld<1152>(base);
+    a[5] ^= lds_peak_ld<1280>(base) ^ lds_peak_ld<1408>(base);
+    a[6] ^= lds_peak_ld<1536>(base) ^ lds_peak_ld<1664>(base);
+    a[7] ^= lds_peak_ld<1792>(base) ^ lds_peak_ld<1920>(base);
+  }
+  const uint32_t x = a[0] ^ a[1] ^ a[2] ^ a[3] ^ a[4] ^ a[5] ^ a[6] ^ a[7];
+  if (x == 0x9E3779B9u) sink[0] = x;  // keep the loads alive
+}
+
 // ---------------------------------------------------------------------------
 // Launchers.
 
@@ -643,6 +675,13 @@ cudaError_t launch_round_probe(const uint32_t* compact, const RoundKeys& rk, uin
   cudaError_t e = set_smem(k_round_probe);
   if (e != cudaSuccess) return e;
   k_round_probe<<<sms, kBlockThreads, kSmemBytes, s>>>(compact, rk, iters, sink);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lds_peak(uint32_t iters, uint32_t* sink, int sms, cudaStream_t s) {
+  cudaError_t e = set_smem(k_lds_peak);
+  if (e != cudaSuccess) return e;
+  k_lds_peak<<<sms, kBlockThreads, kSmemBytes, s>>>(iters, sink);
   return cudaGetLastError();
 }
 

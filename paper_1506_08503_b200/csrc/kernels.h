@@ -33,6 +33,8 @@ cudaError_t launch_bs_blocks(const void* in, void* out, uint64_t n_blocks, const
                              cudaStream_t s);
 cudaError_t launch_round_probe(const uint32_t* compact, const RoundKeys& rk, uint32_t iters, uint32_t* sink,
                                int sms, cudaStream_t s);
+// Shared-memory lookup peak: 16 conflict-free LDS.32 per thread per iteration.
+cudaError_t launch_lds_peak(uint32_t iters, uint32_t* sink, int sms, cudaStream_t s);
 cudaError_t launch_expand_keys(const uint8_t* keys, uint64_t k, const uint32_t* compact_enc, uint8_t* rk_enc,
                                uint8_t* rk_dec, cudaStream_t s);
 cudaError_t launch_many_key(bool dec, const void* in, void* out, uint64_t n_blocks, uint64_t first, uint64_t bpk,

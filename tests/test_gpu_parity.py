@@ -366,8 +366,9 @@ def test_config5_many_key(oracle):
 
 
 def test_launch_counter_and_kernel_name(oracle):
-    before = _lib.launch_count()
     x = torch.zeros((1024, 16), dtype=torch.uint8, device="cuda")
+    device.encrypt_blocks(x, oracle.gen_keys(bytes(16)))  # context (GF-layer build) exists from here on
+    before = _lib.launch_count()
     device.encrypt_blocks(x, oracle.gen_keys(bytes(16)))
     assert _lib.launch_count() == before + 1
     assert _lib.last_kernel().startswith("k_blocks_enc")
@@ -873,3 +874,19 @@ def test_no_out_of_bounds_writes(oracle, n):
                 a = hb.numpy()
                 backend_cuda.cbc_encrypt(ph, ivh, *tables, a[G:G + n * m].reshape(n, m))
                 assert (a[:G] == 0xA5).all() and (a[G + n * m:] == 0xA5).all(), (m, pinned)
+
+
+def test_roofline_probes_are_sane():
+    """The measured LDS peak (roofline denominator) sits near the nominal
+    32 lanes/clk/SM at the max SM clock, and the AES round probe below it."""
+    import ctypes
+    L = _lib.lib()
+    rate, ms = ctypes.c_double(), ctypes.c_double()
+    _lib.check(L.gaes_probe_lds_peak(0, 2048, ctypes.addressof(rate), ctypes.addressof(ms)))
+    lds = rate.value
+    _lib.check(L.gaes_probe_round_rate(0, 128, ctypes.addressof(rate), ctypes.addressof(ms)))
+    rnd = rate.value
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    nominal_max = sms * 32 * 2.1e9  # above any B200 SM clock
+    assert 0.3 * nominal_max < lds < nominal_max
+    assert 0.5 * lds < rnd < 1.02 * lds
