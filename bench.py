@@ -650,6 +650,12 @@ def main():
         except (OSError, ValueError):
             traffic = None
     probe = lds_measured = None
+    # the host-side legs above leave the GPU idle; bring the clocks back to
+    # the timed region's before measuring the roofline denominators
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 0.3:
+        step()
+        torch.cuda.synchronize()
     try:
         import ctypes
         rate, pms = ctypes.c_double(), ctypes.c_double()
