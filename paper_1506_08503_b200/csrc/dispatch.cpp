@@ -269,18 +269,24 @@ int tables_for(DevCtx* c, const uint8_t* box, const uint8_t* lut, uint32_t** out
     for (auto& kv : c->cache) cudaFree(kv.second);
     c->cache.clear();
   }
-  uint32_t* d = nullptr;
-  uint8_t* d_in = nullptr;
-  GAES_CK(cudaMalloc(&d, kCompactWords * 4));
-  GAES_CK(cudaMalloc(&d_in, 256 + 4096));
-  GAES_CK(cudaMemcpy(d_in, box, 256, cudaMemcpyHostToDevice));
-  GAES_CK(cudaMemcpy(d_in + 256, lut, 4096, cudaMemcpyHostToDevice));
-  GAES_CK(launch_build_tables(d_in, d_in + 256, d, 0));
+  struct DevBuf {  // freed on every exit path unless released
+    void* p = nullptr;
+    ~DevBuf() {
+      if (p) cudaFree(p);
+    }
+  } d, d_in;
+  GAES_CK(cudaMalloc(&d.p, kCompactWords * 4));
+  GAES_CK(cudaMalloc(&d_in.p, 256 + 4096));
+  uint8_t* in8 = static_cast<uint8_t*>(d_in.p);
+  GAES_CK(cudaMemcpy(in8, box, 256, cudaMemcpyHostToDevice));
+  GAES_CK(cudaMemcpy(in8 + 256, lut, 4096, cudaMemcpyHostToDevice));
+  GAES_CK(launch_build_tables(in8, in8 + 256, static_cast<uint32_t*>(d.p), 0));
   note_kernel("k_build_tables");
   GAES_CK(cudaDeviceSynchronize());
-  cudaFree(d_in);
-  c->cache.emplace(key, d);
-  *out = d;
+  uint32_t* tables = static_cast<uint32_t*>(d.p);
+  d.p = nullptr;
+  c->cache.emplace(key, tables);
+  *out = tables;
   return GAES_OK;
 }
 
