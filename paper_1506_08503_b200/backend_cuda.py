@@ -102,39 +102,35 @@ def cbc_decrypt(data, ivs, round_keys, inv_sbox, inv_mix_lut, inv_shift_src, out
     return None
 
 
+def _shared_iv(dec: bool, data, iv, round_keys, out):
+    data = _buf(data, "data", 2)
+    rk = _buf(np.ascontiguousarray(round_keys, np.uint8).reshape(11, 16), "round_keys", 2)
+    ivb = np.frombuffer(bytes(iv), np.uint8)
+    if ivb.size != 16:
+        raise ValueError("IV must be 16 bytes")
+    if out is None:
+        out = np.empty_like(data)
+    out = _buf(out, "out", 2, writable=True)
+    if out.shape != data.shape:
+        raise ValueError(f"out shape {out.shape} does not match data shape {data.shape}")
+    n, m = data.shape
+    if n:
+        fn = _lib.lib().gaes_decrypt_shared_iv if dec else _lib.lib().gaes_encrypt_shared_iv
+        _lib.check(fn(_ptr(data), n, m, _ptr(ivb), _ptr(rk), _ptr(out)))
+    return out
+
+
 def encrypt_shared_iv(data: np.ndarray, iv: bytes, round_keys, out: np.ndarray | None = None) -> np.ndarray:
     """Host-buffer encrypt with one shared IV (no N x 16 IV grid crosses PCIe).
 
     Same bytes as ``encrypt_batch(key, IVSet.shared(iv), batch)`` for
     ``round_keys = gen_keys(key, S).to_array()``.
     """
-    data = _buf(data, "data", 2)
-    rk = _buf(np.ascontiguousarray(round_keys, np.uint8).reshape(11, 16), "round_keys", 2)
-    ivb = np.frombuffer(bytes(iv), np.uint8)
-    if ivb.size != 16:
-        raise ValueError("IV must be 16 bytes")
-    if out is None:
-        out = np.empty_like(data)
-    out = _buf(out, "out", 2, writable=True)
-    n, m = data.shape
-    if n:
-        _lib.check(_lib.lib().gaes_encrypt_shared_iv(_ptr(data), n, m, _ptr(ivb), _ptr(rk), _ptr(out)))
-    return out
+    return _shared_iv(False, data, iv, round_keys, out)
 
 
 def decrypt_shared_iv(data: np.ndarray, iv: bytes, round_keys, out: np.ndarray | None = None) -> np.ndarray:
-    data = _buf(data, "data", 2)
-    rk = _buf(np.ascontiguousarray(round_keys, np.uint8).reshape(11, 16), "round_keys", 2)
-    ivb = np.frombuffer(bytes(iv), np.uint8)
-    if ivb.size != 16:
-        raise ValueError("IV must be 16 bytes")
-    if out is None:
-        out = np.empty_like(data)
-    out = _buf(out, "out", 2, writable=True)
-    n, m = data.shape
-    if n:
-        _lib.check(_lib.lib().gaes_decrypt_shared_iv(_ptr(data), n, m, _ptr(ivb), _ptr(rk), _ptr(out)))
-    return out
+    return _shared_iv(True, data, iv, round_keys, out)
 
 
 def cbc_encrypt_std(data, ivs, round_keys, out=None) -> np.ndarray:

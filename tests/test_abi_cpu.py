@@ -107,6 +107,32 @@ def test_backend_argument_errors(lib, oracle):
                              np.empty((0, 16), np.uint8))
 
 
+def test_host_entry_shape_errors_before_any_device_call(lib):
+    """Every host entry point validates shapes in Python, before the C ABI
+    (an `out` smaller than `data` must never reach a kernel or a copy)."""
+    from paper_1506_08503_b200 import backend_cuda
+    rk = np.zeros((11, 16), np.uint8)
+    data = np.zeros((8, 16), np.uint8)
+    short = np.zeros((4, 16), np.uint8)
+    for fn in (backend_cuda.encrypt_shared_iv, backend_cuda.decrypt_shared_iv):
+        with pytest.raises(ValueError, match="does not match"):
+            fn(data, bytes(16), rk, out=short)
+        with pytest.raises(ValueError, match="16 bytes"):
+            fn(data, bytes(15), rk)
+    for fn in (backend_cuda.cbc_encrypt_std, backend_cuda.cbc_decrypt_std):
+        with pytest.raises(ValueError, match="must match"):
+            fn(data, np.zeros((8, 16), np.uint8), rk, out=short)
+        with pytest.raises(ValueError, match="N x 16"):
+            fn(data, np.zeros((7, 16), np.uint8), rk)
+    for fn in (backend_cuda.many_key_encrypt, backend_cuda.many_key_decrypt):
+        with pytest.raises(ValueError, match="must match"):
+            fn(data, np.zeros((2, 16), np.uint8), out=short)
+        with pytest.raises(ValueError, match="multiple of K"):
+            fn(data, np.zeros((3, 16), np.uint8))
+        with pytest.raises(ValueError, match="K x 16"):
+            fn(data, np.zeros((2, 16), np.uint8), np.zeros((3, 16), np.uint8))
+
+
 def test_product_package_does_not_import_the_oracle():
     pkg = os.path.join(REPO, "paper_1506_08503_b200")
     for root, _, files in os.walk(pkg):
@@ -126,3 +152,18 @@ def test_c_example_links_against_the_abi(lib, tmp_path):
                            os.path.join(REPO, "examples", "encrypt_c.c"), "-L", os.path.dirname(lib.LIB_PATH),
                            "-lgaes_b200", f"-Wl,-rpath,{os.path.dirname(lib.LIB_PATH)}", "-o", str(exe)])
     assert exe.exists()
+
+
+def test_device_api_rejects_host_tensors(lib):
+    """The device-resident API takes CUDA tensors only -- it never copies a
+    host tensor to the device behind the caller's back (no silent fallback)."""
+    torch = pytest.importorskip("torch")
+    from paper_1506_08503_b200 import device
+    x = torch.zeros((4, 16), dtype=torch.uint8)
+    rk = np.zeros((11, 16), np.uint8)
+    for call in (lambda: device.encrypt_blocks(x, rk), lambda: device.decrypt_blocks(x, rk),
+                 lambda: device.cbc_encrypt(x, rk), lambda: device.cbc_decrypt(x, rk),
+                 lambda: device.expand_keys(x), lambda: device.BlockCipher(rk).encrypt(x),
+                 lambda: device.many_key_encrypt(x, torch.zeros((1, 11, 16), dtype=torch.uint8))):
+        with pytest.raises(ValueError):
+            call()
