@@ -482,6 +482,14 @@ struct Job {
   size_t bpk = 0, first = 0, n_keys = 0;
   const uint8_t* mk_keys = nullptr;
   const uint8_t* mk_ivs = nullptr;
+  // auto_iv (pageable drop-in calls): `ivs` may be IVSet.rows' tiling of one
+  // IV.  Each staged chunk checks its rows against iv0 while it is copied;
+  // chunks that match run the shared variant (mode_shared / rk_shared, no IV
+  // rows cross PCIe), the others the per-row variant (mode / rk / ivs).
+  bool auto_iv = false;
+  const uint8_t* iv0 = nullptr;
+  Mode mode_shared = Mode::kFolded;
+  RoundKeys rk_shared;
 };
 
 bool is_pinned(const void* p) {
@@ -599,6 +607,32 @@ int launch_chunk(DevCtx* c, const Job& j, cudaStream_t stream, const uint8_t* in
     }
   }
   return GAES_OK;
+}
+
+// One parallel pass over a staged chunk: copy rows [0, rows) of width m to
+// the pinned staging buffer and check that their IV rows all equal iv0
+// (IVSet.rows tiles a shared IV, aes_cbc.py:107-115).  Fusing the check into
+// the copy keeps the IV grid off the critical path: no whole-grid pre-scan
+// before the first chunk.
+bool stage_and_check_iv(uint8_t* dst, const uint8_t* src, size_t m, const uint8_t* ivs, size_t rows,
+                        const uint8_t* iv0) {
+  std::atomic<bool> same{true};
+  uint64_t a0, a1;
+  std::memcpy(&a0, iv0, 8);
+  std::memcpy(&a1, iv0 + 8, 8);
+  parallel_ranges(rows, std::max<size_t>(1, ((size_t)128 << 10) / m), [&](size_t lo, size_t hi) {
+    std::memcpy(dst + lo * m, src + lo * m, (hi - lo) * m);
+    if (!same.load(std::memory_order_relaxed)) return;
+    uint64_t diff = 0;
+    for (size_t i = lo; i < hi; i++) {
+      uint64_t b0, b1;
+      std::memcpy(&b0, ivs + 16 * i, 8);
+      std::memcpy(&b1, ivs + 16 * i + 8, 8);
+      diff |= (a0 ^ b0) | (a1 ^ b1);
+    }
+    if (diff) same.store(false, std::memory_order_relaxed);
+  });
+  return same.load();
 }
 
 // Runs rows [0, j.n) of `j` on device context c (one shard).
@@ -736,12 +770,25 @@ int run_job(DevCtx* c, const Job& j) {
     const size_t rows = chunks[ci].second;
     const size_t off = r0 * j.m, bytes = rows * j.m;
     const uint8_t* src = j.data + off;
+    bool chunk_shared = false;
     if (!in_pinned) {
-      par_memcpy(s.h_in, src, bytes);
+      if (j.auto_iv)
+        chunk_shared = stage_and_check_iv(s.h_in, src, j.m, j.ivs + r0 * 16, rows, j.iv0);
+      else
+        par_memcpy(s.h_in, src, bytes);
       src = s.h_in;
     }
     GAES_CK(cudaMemcpyAsync(s.d_in, src, bytes, cudaMemcpyHostToDevice, s.stream));
-    if (need_iv) {
+    Job shared_view;
+    const Job* jc = &j;
+    if (chunk_shared) {
+      shared_view = j;
+      shared_view.mode = j.mode_shared;
+      shared_view.rk = j.rk_shared;
+      shared_view.ivs = nullptr;
+      jc = &shared_view;
+    }
+    if (need_iv && !chunk_shared) {
       const uint8_t* ivsrc = j.ivs + r0 * 16;
       if (!iv_pinned) {
         par_memcpy(s.h_iv, ivsrc, rows * 16);
@@ -749,7 +796,7 @@ int run_job(DevCtx* c, const Job& j) {
       }
       GAES_CK(cudaMemcpyAsync(s.d_iv, ivsrc, rows * 16, cudaMemcpyHostToDevice, s.stream));
     }
-    int rc = launch_chunk(c, j, s.stream, s.d_in, s.d_out, s.d_iv, r0, rows, compact,
+    int rc = launch_chunk(c, *jc, s.stream, s.d_in, s.d_out, s.d_iv, r0, rows, compact,
                           tex_for(c, s.d_in, s.cap, s.stream));
     if (rc) return rc;
     if (out_pinned) {
@@ -888,7 +935,23 @@ int cbc_host(bool dec, const uint8_t* data, const uint8_t* ivs, size_t n, size_t
     return run_sharded(j);
   }
   const size_t bpr = m / 16;
-  if (n >= ((size_t)1 << 14)) host_pool().warm();  // parallel IV scan + staging copies follow
+  if (n >= ((size_t)1 << 14)) host_pool().warm();  // parallel IV checks + staging copies follow
+  if (!is_pinned(data)) {
+    // staged input: the shared-IV check rides along with each chunk's copy
+    j.auto_iv = true;
+    j.iv0 = ivs;
+    j.ivs = ivs;
+    if (dec || bpr == 1) {
+      j.mode = Mode::kChain;
+      j.rk = dec ? make_dec_keys(rk, ivs, false, lut) : make_enc_keys(rk, ivs, false);
+    } else {
+      j.mode = Mode::kEncRows;
+      j.rk = make_enc_keys(rk, ivs, false);
+    }
+    j.mode_shared = bpr == 1 ? Mode::kFolded : j.mode;
+    j.rk_shared = bpr != 1 ? j.rk : dec ? make_dec_keys(rk, ivs, true, lut) : make_enc_keys(rk, ivs, true);
+    return run_sharded(j);
+  }
   const bool shared = rows_share_iv(ivs, n);
   if (bpr == 1 && shared) {
     j.mode = Mode::kFolded;

@@ -890,3 +890,26 @@ def test_roofline_probes_are_sane():
     nominal_max = sms * 32 * 2.1e9  # above any B200 SM clock
     assert 0.3 * nominal_max < lds < nominal_max
     assert 0.5 * lds < rnd < 1.02 * lds
+
+
+@pytest.mark.parametrize("m", [16, 48])
+def test_dropin_mixed_shared_and_per_row_iv_chunks(oracle, m):
+    """Pageable drop-in calls check IV rows per staged chunk: a grid whose IV
+    rows are the tiled shared IV except for one stretch must give the oracle's
+    bytes, with chunks before/after the stretch on the shared-IV kernels and
+    the chunk holding it on the per-row kernels."""
+    rng = np.random.default_rng(m)
+    key = rng.bytes(16)
+    n = 600000 if m == 16 else 200000
+    data = rng.integers(0, 256, (n, m), dtype=np.uint8)
+    iv0 = rng.integers(0, 256, 16, dtype=np.uint8)
+    ivs = np.tile(iv0, (n, 1))
+    lo = n // 4
+    ivs[lo:lo + 10000] = rng.integers(0, 256, (10000, 16), dtype=np.uint8)
+    want = oracle.encrypt(key, ivs, data, threads=8)
+    out = np.empty_like(data)
+    backend_cuda.cbc_encrypt(data, ivs, *oracle.encrypt_tables(key), out)
+    assert np.array_equal(out, want)
+    back = np.empty_like(data)
+    backend_cuda.cbc_decrypt(out, ivs, *oracle.decrypt_tables(key), back)
+    assert np.array_equal(back, data)
