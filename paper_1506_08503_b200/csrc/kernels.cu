@@ -151,17 +151,28 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
       const uint64_t bk = b + k * T;
       uint4 x = make_uint4(0, 0, 0, 0);
       if (IVM == kIvChain) {
-        // The previous ciphertext block is lane-1's current block (lanes
-        // hold consecutive blocks); lane 0 reads it from memory.
-        uint4 prev;
-        prev.x = __shfl_up_sync(0xFFFFFFFFu, cur[k].x, 1);
-        prev.y = __shfl_up_sync(0xFFFFFFFFu, cur[k].y, 1);
-        prev.z = __shfl_up_sync(0xFFFFFFFFu, cur[k].z, 1);
-        prev.w = __shfl_up_sync(0xFFFFFFFFu, cur[k].w, 1);
-        if (bk < n_blocks) {
-          if (jj[k]) x = lane ? prev : __ldg(in + bk - 1);
-          else if (ivs) x = __ldg(ivs + row[k]);
-          else x = make_uint4(rk.iv[0], rk.iv[1], rk.iv[2], rk.iv[3]);
+        if (TEXIN) {
+          // The previous ciphertext block comes through the texture path
+          // too (a cache hit: the neighbouring lane fetched it), keeping
+          // the shuffles and lane 0's extra load off the L1 data pipe.
+          if (bk < n_blocks) {
+            if (jj[k]) x = tex1Dfetch<uint4>(tin, (int)(bk - 1));
+            else if (ivs) x = __ldg(ivs + row[k]);
+            else x = make_uint4(rk.iv[0], rk.iv[1], rk.iv[2], rk.iv[3]);
+          }
+        } else {
+          // The previous ciphertext block is lane-1's current block (lanes
+          // hold consecutive blocks); lane 0 reads it from memory.
+          uint4 prev;
+          prev.x = __shfl_up_sync(0xFFFFFFFFu, cur[k].x, 1);
+          prev.y = __shfl_up_sync(0xFFFFFFFFu, cur[k].y, 1);
+          prev.z = __shfl_up_sync(0xFFFFFFFFu, cur[k].z, 1);
+          prev.w = __shfl_up_sync(0xFFFFFFFFu, cur[k].w, 1);
+          if (bk < n_blocks) {
+            if (jj[k]) x = lane ? prev : __ldg(in + bk - 1);
+            else if (ivs) x = __ldg(ivs + row[k]);
+            else x = make_uint4(rk.iv[0], rk.iv[1], rk.iv[2], rk.iv[3]);
+          }
         }
         jj[k] += adv_mod;
         row[k] += adv_div;

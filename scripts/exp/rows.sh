@@ -1,6 +1,6 @@
-set -e
-python -m pytest tests -x -q -m gpu -k "probes or launch_counter" 2>&1 | tail -2
-python bench.py --no-cpu-baseline > gpurun_out/b2.json
-python -c "
-import json
-d = json.load(open('gpurun_out/b2.json')); print(json.dumps(d['roofline'], indent=1)); print(d['clocks'])"
+python -m pytest tests -x -q -m gpu -k "cbc or grid or iv or aliased or in_place or dropin_mixed" 2>&1 | tail -2
+for i in 1 2; do
+python scripts/profile_kernels.py cbc_dec_rows 24 64
+python scripts/profile_kernels.py cbc_dec_rows 24 1
+python scripts/profile_kernels.py cbc_dec_rows 24 4
+done
