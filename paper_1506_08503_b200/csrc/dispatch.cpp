@@ -562,7 +562,8 @@ int finish_slot(Slot& s) {
 // hold exactly those rows (device staging buffers, or the caller's pinned
 // host buffers for a zero-copy launch); `tin` is a texture over `in` or 0.
 int launch_chunk(DevCtx* c, const Job& j, cudaStream_t stream, const uint8_t* in, uint8_t* out,
-                 const uint8_t* ivs, size_t r0, size_t rows, const uint32_t* compact, cudaTextureObject_t tin) {
+                 const uint8_t* ivs, size_t r0, size_t rows, const uint32_t* compact, cudaTextureObject_t tin,
+                 cudaTextureObject_t tiv = 0) {
   const uint64_t bpr = j.m / 16;
   const uint64_t nblk = rows * bpr;
   switch (j.mode) {
@@ -582,7 +583,7 @@ int launch_chunk(DevCtx* c, const Job& j, cudaStream_t stream, const uint8_t* in
       break;
     case Mode::kChain:
       GAES_CK(launch_blocks(j.dec, kIvChain, ilp_default(), in, out, nblk, compact, j.rk,
-                            j.ivs ? ivs : nullptr, bpr, c->sms, stream, tin));
+                            j.ivs ? ivs : nullptr, bpr, c->sms, stream, tin, j.ivs ? tiv : 0));
       note_kernel(j.dec ? "k_blocks_dec_chain" : "k_blocks_enc_chain");
       break;
     case Mode::kEncRows:
@@ -796,8 +797,10 @@ int run_job(DevCtx* c, const Job& j) {
       }
       GAES_CK(cudaMemcpyAsync(s.d_iv, ivsrc, rows * 16, cudaMemcpyHostToDevice, s.stream));
     }
+    const bool iv_tex = jc->ivs && jc->mode == Mode::kChain && j.m == 16;
     int rc = launch_chunk(c, *jc, s.stream, s.d_in, s.d_out, s.d_iv, r0, rows, compact,
-                          tex_for(c, s.d_in, s.cap, s.stream));
+                          tex_for(c, s.d_in, s.cap, s.stream),
+                          iv_tex ? tex_for(c, s.d_iv, s.iv_cap, s.stream) : TexLease());
     if (rc) return rc;
     if (out_pinned) {
       GAES_CK(cudaMemcpyAsync(j.out + off, s.d_out, bytes, cudaMemcpyDeviceToHost, s.stream));
@@ -1268,7 +1271,8 @@ GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m,
   if (rc) return rc;
   if (bpr == 1) {
     GAES_CK(launch_blocks(false, kIvChain, ilp_default(), src, out, n, c->d_std_enc, k, ivs_dev, 1, c->sms,
-                          (cudaStream_t)stream, tex_for(c, src, n * 16, (cudaStream_t)stream)));
+                          (cudaStream_t)stream, tex_for(c, src, n * 16, (cudaStream_t)stream),
+                          tex_for(c, ivs_dev, n * 16, (cudaStream_t)stream)));
     note_kernel("k_blocks_enc_chain");
   } else {
     // segments of whole rows, each inside one texture
@@ -1303,7 +1307,8 @@ GAES_API int gaes_cbc_decrypt_dev(const void* in, void* out, size_t n, size_t m,
   rc = private_input_if_aliased(in, out, n * m, bpr > 1, (cudaStream_t)stream, &src, &tmp);
   if (rc) return rc;
   GAES_CK(launch_blocks(true, kIvChain, ilp_default(), src, out, n * bpr, c->d_std_dec, k, ivs_dev, bpr, c->sms,
-                        (cudaStream_t)stream, tex_for(c, src, n * bpr * 16, (cudaStream_t)stream)));
+                        (cudaStream_t)stream, tex_for(c, src, n * bpr * 16, (cudaStream_t)stream),
+                        bpr == 1 && ivs_dev ? tex_for(c, ivs_dev, n * 16, (cudaStream_t)stream) : TexLease()));
   note_kernel("k_blocks_dec_chain");
   return GAES_OK;
 }

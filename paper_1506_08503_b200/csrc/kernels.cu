@@ -97,6 +97,9 @@ __device__ __forceinline__ void st_stream(uint4* p, uint4 v) { __stcs(p, v); }
 //                     x = j ? in[b-1] : (ivs ? ivs[i] : rk.iv).
 //                     encrypt: state ^= x (only valid for bpr == 1);
 //                     decrypt: out ^= x.
+//   IVM == kIvRows  : one block per row with its own IV: x = ivs[b] (no
+//                     row tracking), fetched through the texture `tiv`
+//                     when one is given (IVSet.per_message, aes_cbc.py:96-105).
 //   TEXIN: the 16-byte input loads go through the texture path
 //          (tex1Dfetch on a linear texture over `in`) instead of LDG: the
 //          L1/shared data pipe the table lookups saturate then carries only
@@ -106,7 +109,7 @@ template <int ILP, bool DEC, int IVM, bool TEXIN = false>
 __global__ void __launch_bounds__(kBlockThreads, 1)
     k_blocks(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks,
              const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
-             const uint4* __restrict__ ivs, uint64_t bpr, cudaTextureObject_t tin) {
+             const uint4* __restrict__ ivs, uint64_t bpr, cudaTextureObject_t tin, cudaTextureObject_t tiv) {
   extern __shared__ __align__(1024) char smem[];
   // Warp-interleaved block map: warp w of CTA c owns the 32 consecutive
   // blocks starting at 32 (w * gridDim + c), so a batch smaller than the
@@ -150,6 +153,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
     for (int k = 0; k < ILP; k++) {
       const uint64_t bk = b + k * T;
       uint4 x = make_uint4(0, 0, 0, 0);
+      if (IVM == kIvRows && bk < n_blocks) x = tiv ? tex1Dfetch<uint4>(tiv, (int)bk) : __ldg(ivs + bk);
       if (IVM == kIvChain) {
         if (TEXIN) {
           // The previous ciphertext block comes through the texture path
@@ -587,20 +591,31 @@ cudaError_t launch_build_tables(const uint8_t* box, const uint8_t* lut, uint32_t
 template <int ILP, bool DEC, int IVM, bool TEXIN = false>
 static cudaError_t launch_blocks_t(const void* in, void* out, uint64_t n, const uint32_t* compact,
                                    const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms, cudaStream_t s,
-                                   cudaTextureObject_t tin = 0) {
+                                   cudaTextureObject_t tin = 0, cudaTextureObject_t tiv = 0) {
   auto kern = k_blocks<ILP, DEC, IVM, TEXIN>;
   cudaError_t e = set_smem(kern);
   if (e != cudaSuccess) return e;
   // every SM that gets at least one warp's 32 blocks (see k_blocks' map)
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(sms, (n + 31) / 32));
   return launch_pdl(kern, grid, kBlockThreads, kSmemBytes, s, (const uint4*)in, (uint4*)out, n, compact, rk,
-                    (const uint4*)ivs, bpr, tin);
+                    (const uint4*)ivs, bpr, tin, tiv);
 }
 
 cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* out, uint64_t n_blocks,
                           const uint32_t* compact, const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms,
-                          cudaStream_t s, cudaTextureObject_t tin) {
+                          cudaStream_t s, cudaTextureObject_t tin, cudaTextureObject_t tiv) {
   if (n_blocks == 0) return cudaSuccess;
+  if (ivmode == kIvChain && bpr == 1 && ivs) ivmode = kIvRows;  // per-row IVs, one block per row
+  if (n_blocks > 0x7FFFFFFFull) tiv = 0;
+  if (ivmode == kIvRows) {
+    if (!(tin && n_blocks <= 0x7FFFFFFFull)) tin = 0;
+    if (tin) {
+      if (dec) return launch_blocks_t<1, true, kIvRows, true>(in, out, n_blocks, compact, rk, ivs, 1, sms, s, tin, tiv);
+      return launch_blocks_t<1, false, kIvRows, true>(in, out, n_blocks, compact, rk, ivs, 1, sms, s, tin, tiv);
+    }
+    if (dec) return launch_blocks_t<1, true, kIvRows, false>(in, out, n_blocks, compact, rk, ivs, 1, sms, s, 0, tiv);
+    return launch_blocks_t<1, false, kIvRows, false>(in, out, n_blocks, compact, rk, ivs, 1, sms, s, 0, tiv);
+  }
   if (tin && n_blocks <= 0x7FFFFFFFull) {
     if (ivmode == kIvFolded) {
       if (dec) return launch_blocks_t<1, true, kIvFolded, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin);

@@ -14,14 +14,15 @@ static constexpr int kBsThreads = 128;         // k_bs_blocks: ~170 registers pe
 static constexpr int kBsCtasPerSm = 3;
 static constexpr int kIvFolded = 0;
 static constexpr int kIvChain = 1;
+static constexpr int kIvRows = 2;  // internal: kIvChain with bpr == 1 and per-row IVs
 
 cudaError_t launch_gf_build(uint32_t* enc, uint32_t* dec, uint8_t* sbox, uint8_t* inv, int* err, cudaStream_t s);
 cudaError_t launch_build_tables(const uint8_t* box, const uint8_t* lut, uint32_t* out, cudaStream_t s);
-// tin: optional linear texture over `in` (uint4 texels) for the folded
-// modes; 0 = plain LDG.
+// tin: optional linear texture over `in` (uint4 texels); tiv: optional
+// texture over `ivs` (per-row IVs with one block per row); 0 = plain LDG.
 cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* out, uint64_t n_blocks,
                           const uint32_t* compact, const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms,
-                          cudaStream_t s, cudaTextureObject_t tin = 0);
+                          cudaStream_t s, cudaTextureObject_t tin = 0, cudaTextureObject_t tiv = 0);
 cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint64_t bpr, const uint32_t* compact,
                                 const RoundKeys& rk, const void* ivs, int sms, cudaStream_t s,
                                 cudaTextureObject_t tin = 0);

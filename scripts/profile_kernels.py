@@ -1,6 +1,6 @@
 """Run one hot-path op a few times on cuda:0 (a small target for ncu).
 
-    python scripts/profile_kernels.py {encrypt,decrypt,bitsliced,manykey,cbc_rows,cbc_dec_rows} [log2_blocks] [bpr]
+    python scripts/profile_kernels.py {encrypt,decrypt,bitsliced,manykey,cbc_rows,cbc_dec_rows,rowiv_enc,rowiv_dec} [log2_blocks] [bpr]
 """
 import sys
 
@@ -17,6 +17,7 @@ rng = np.random.default_rng(2016)
 key, iv = rng.bytes(16), rng.bytes(16)
 rk = device.expand_key(key)
 x = torch.randint(0, 256, (n, 16), dtype=torch.uint8, device="cuda")
+ivs = torch.randint(0, 256, (n, 16), dtype=torch.uint8, device="cuda") if op.startswith("rowiv") else None
 def run():
     if op == "encrypt":
         device.encrypt_blocks(x, rk, iv)
@@ -29,6 +30,10 @@ def run():
         device.cbc_encrypt(x.view(n // bpr, bpr * 16), rk, iv)
     elif op == "cbc_dec_rows":
         device.cbc_decrypt(x.view(n // bpr, bpr * 16), rk, iv)
+    elif op == "rowiv_enc":  # M = 16 with per-message IVs (IVSet.per_message)
+        device.cbc_encrypt(x, rk, ivs)
+    elif op == "rowiv_dec":
+        device.cbc_decrypt(x, rk, ivs)
 
 
 if op == "manykey":
