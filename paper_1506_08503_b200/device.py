@@ -22,8 +22,19 @@ import torch
 from . import _lib
 
 
-def _stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def _stream(device_index: int | None = None) -> int:
+    """Raw handle of torch's current stream on `device_index` (default: the
+    current device).  torch._C._cuda_getCurrentRawStream costs ~0.06 us,
+    torch.cuda.current_stream().cuda_stream ~3 us -- a third of a small
+    call's host time."""
+    if device_index is None:
+        device_index = torch.cuda.current_device()
+    if _raw_stream is not None:
+        return _raw_stream(device_index)
+    return torch.cuda.current_stream(device_index).cuda_stream
 
 
 def _u8_cuda(t: torch.Tensor, name: str, ndim: int | None = None) -> torch.Tensor:
@@ -112,11 +123,12 @@ class BlockCipher:
             out = torch.empty_like(x)
         elif out.shape != x.shape or out.device != x.device or out.dtype != torch.uint8 or not out.is_contiguous():
             raise ValueError("out must match the input")
-        if x.device.index != torch.cuda.current_device():
+        dev = x.get_device()
+        if dev != torch.cuda.current_device():
             with _on_device(x.device):
-                _lib.check(fn(x.data_ptr(), out.data_ptr(), x.shape[0], self._rk_p, self._iv_p, _stream()))
+                _lib.check(fn(x.data_ptr(), out.data_ptr(), x.shape[0], self._rk_p, self._iv_p, _stream(dev)))
         else:
-            _lib.check(fn(x.data_ptr(), out.data_ptr(), x.shape[0], self._rk_p, self._iv_p, _stream()))
+            _lib.check(fn(x.data_ptr(), out.data_ptr(), x.shape[0], self._rk_p, self._iv_p, _stream(dev)))
         return out
 
     def encrypt(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
