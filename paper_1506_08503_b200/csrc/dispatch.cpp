@@ -82,22 +82,33 @@ struct Slot {
 };
 
 constexpr int kSlots = 4;
+constexpr int kLanes = 4;
+
+// One host-buffer job at a time runs on a lane: its staging slots and
+// streams plus the per-job device scratch.  Several lanes per device let
+// concurrent callers (the reference's parallel._run_chunks worker threads,
+// parallel.py:66-75) overlap their host copies, transfers and kernels
+// instead of queueing behind one device mutex.
+struct Lane {
+  std::mutex mu;
+  Slot slots[kSlots];
+  uint8_t* d_scratch = nullptr;  // generic path: box(256) lut(4096) perm(16) rk(176)
+  uint8_t* d_mk = nullptr;       // many-key: keys | rk_enc | rk_dec | ivs
+  size_t mk_cap = 0;
+  uint32_t* d_tables = nullptr;  // caller tables built here once the per-device cache is full
+};
 
 struct DevCtx {
   int dev = 0;
   int sms = 148;
-  std::mutex mu;  // serialises host-API use of the staging slots
   uint32_t* d_std_enc = nullptr;  // compact 5x256 (GF layer)
   uint32_t* d_std_dec = nullptr;
   uint8_t std_sbox[256], std_inv[256];
   uint32_t std_te[1024], std_td[1024];
   uint8_t std_mix_fwd[4096], std_mix_inv[4096];  // mix_lut[r][j][x] = M[r][j] * x
   std::mutex cache_mu;
-  std::unordered_map<std::string, uint32_t*> cache;  // (box || lut) -> compact tables
-  uint8_t* d_scratch = nullptr;  // box(256) lut(4096) perm(16) rk(176)
+  std::unordered_map<std::string, uint32_t*> cache;  // (box || lut) -> compact tables; never evicted
   uint8_t* d_tmp = nullptr;      // GF-build outputs + error flag
-  uint8_t* d_mk = nullptr;       // many-key: keys | rk (K x 176) | ivs
-  size_t mk_cap = 0;
   // linear textures over input buffers (texture-path loads, see k_blocks),
   // least-recently-used first; see tex_for
   struct Tex {
@@ -113,15 +124,19 @@ struct DevCtx {
   uint64_t tex_clock = 0;
   int tex_align = 0;
   size_t tex_max_texels = 0;
-  Slot slots[kSlots];
+  Lane lanes[kLanes];
   // Only runs when initialisation fails (live contexts are never destroyed:
   // freeing after the CUDA runtime has shut down at exit is not allowed).
   ~DevCtx() {
-    for (void* p : {(void*)d_std_enc, (void*)d_std_dec, (void*)d_scratch, (void*)d_tmp, (void*)d_mk})
+    for (void* p : {(void*)d_std_enc, (void*)d_std_dec, (void*)d_tmp})
       if (p) cudaFree(p);
-    for (auto& s : slots) {
-      if (s.stream) cudaStreamDestroy(s.stream);
-      if (s.done) cudaEventDestroy(s.done);
+    for (auto& L : lanes) {
+      for (void* p : {(void*)L.d_scratch, (void*)L.d_mk, (void*)L.d_tables})
+        if (p) cudaFree(p);
+      for (auto& s : L.slots) {
+        if (s.stream) cudaStreamDestroy(s.stream);
+        if (s.done) cudaEventDestroy(s.done);
+      }
     }
     for (auto& kv : cache) cudaFree(kv.second);
     for (auto& t : tex_cache) {
@@ -196,7 +211,6 @@ int get_ctx(int dev, DevCtx** out) {
   GAES_CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->dev));
   GAES_CK(cudaMalloc(&c->d_std_enc, kCompactWords * 4));
   GAES_CK(cudaMalloc(&c->d_std_dec, kCompactWords * 4));
-  GAES_CK(cudaMalloc(&c->d_scratch, 256 + 4096 + 16 + 176 + 512));
   GAES_CK(cudaMalloc(&c->d_tmp, 512 + sizeof(int)));
   uint8_t* d_box = c->d_tmp;
   int* d_err = reinterpret_cast<int*>(c->d_tmp + 512);
@@ -212,9 +226,12 @@ int get_ctx(int dev, DevCtx** out) {
   std::memcpy(c->std_te, tmp, sizeof(c->std_te));
   GAES_CK(cudaMemcpy(tmp, c->d_std_dec, sizeof(tmp), cudaMemcpyDeviceToHost));
   std::memcpy(c->std_td, tmp, sizeof(c->std_td));
-  for (auto& s : c->slots) {
-    GAES_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
-    GAES_CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+  for (auto& L : c->lanes) {
+    GAES_CK(cudaMalloc(&L.d_scratch, 256 + 4096 + 16 + 176 + 512));
+    for (auto& s : L.slots) {
+      GAES_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+      GAES_CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    }
   }
   if (err) return fail(GAES_ETABLE, "GF layer self check failed (S^-1 o S != id or M.M^-1 != I)");
   // The device-built S-box must equal the host restatement of the same
@@ -254,8 +271,12 @@ int current_ctx(DevCtx** out) {
   return fail(GAES_EINVAL, "current device is not in GAES_DEVICE_MAP");
 }
 
-// Compact T tables for caller-supplied (box, lut), cached per device.
-int tables_for(DevCtx* c, const uint8_t* box, const uint8_t* lut, uint32_t** out) {
+// Compact T tables for caller-supplied (box, lut), cached per device (up to
+// 64 sets, never evicted: a concurrent job may be about to launch with any
+// cached pointer).  Past that, the tables are built into the lane's own
+// buffer for this job.  `stream` is the lane's stream.
+int tables_for(DevCtx* c, Lane* lane, cudaStream_t stream, const uint8_t* box, const uint8_t* lut,
+               uint32_t** out) {
   std::string key(reinterpret_cast<const char*>(box), 256);
   key.append(reinterpret_cast<const char*>(lut), 4096);
   std::lock_guard<std::mutex> lk(c->cache_mu);
@@ -264,28 +285,32 @@ int tables_for(DevCtx* c, const uint8_t* box, const uint8_t* lut, uint32_t** out
     *out = it->second;
     return GAES_OK;
   }
-  if (c->cache.size() >= 64) {  // bounded: drop everything (tables are cheap to rebuild)
-    GAES_CK(cudaDeviceSynchronize());
-    for (auto& kv : c->cache) cudaFree(kv.second);
-    c->cache.clear();
-  }
+  const bool cache_it = c->cache.size() < 64;
   struct DevBuf {  // freed on every exit path unless released
     void* p = nullptr;
     ~DevBuf() {
       if (p) cudaFree(p);
     }
   } d, d_in;
-  GAES_CK(cudaMalloc(&d.p, kCompactWords * 4));
+  uint32_t* tables = nullptr;
+  if (cache_it) {
+    GAES_CK(cudaMalloc(&d.p, kCompactWords * 4));
+    tables = static_cast<uint32_t*>(d.p);
+  } else {
+    if (!lane->d_tables) GAES_CK(cudaMalloc(&lane->d_tables, kCompactWords * 4));
+    tables = lane->d_tables;
+  }
   GAES_CK(cudaMalloc(&d_in.p, 256 + 4096));
   uint8_t* in8 = static_cast<uint8_t*>(d_in.p);
-  GAES_CK(cudaMemcpy(in8, box, 256, cudaMemcpyHostToDevice));
-  GAES_CK(cudaMemcpy(in8 + 256, lut, 4096, cudaMemcpyHostToDevice));
-  GAES_CK(launch_build_tables(in8, in8 + 256, static_cast<uint32_t*>(d.p), 0));
+  GAES_CK(cudaMemcpyAsync(in8, box, 256, cudaMemcpyHostToDevice, stream));
+  GAES_CK(cudaMemcpyAsync(in8 + 256, lut, 4096, cudaMemcpyHostToDevice, stream));
+  GAES_CK(launch_build_tables(in8, in8 + 256, tables, stream));
   note_kernel("k_build_tables");
-  GAES_CK(cudaDeviceSynchronize());
-  uint32_t* tables = static_cast<uint32_t*>(d.p);
-  d.p = nullptr;
-  c->cache.emplace(key, tables);
+  GAES_CK(cudaStreamSynchronize(stream));
+  if (cache_it) {
+    d.p = nullptr;
+    c->cache.emplace(key, tables);
+  }
   *out = tables;
   return GAES_OK;
 }
@@ -561,7 +586,7 @@ int finish_slot(Slot& s) {
 // One kernel launch over rows [r0, r0 + rows) of job j: `in` / `out` / `ivs`
 // hold exactly those rows (device staging buffers, or the caller's pinned
 // host buffers for a zero-copy launch); `tin` is a texture over `in` or 0.
-int launch_chunk(DevCtx* c, const Job& j, cudaStream_t stream, const uint8_t* in, uint8_t* out,
+int launch_chunk(DevCtx* c, Lane* lane, const Job& j, cudaStream_t stream, const uint8_t* in, uint8_t* out,
                  const uint8_t* ivs, size_t r0, size_t rows, const uint32_t* compact, cudaTextureObject_t tin,
                  cudaTextureObject_t tiv = 0) {
   const uint64_t bpr = j.m / 16;
@@ -594,13 +619,13 @@ int launch_chunk(DevCtx* c, const Job& j, cudaStream_t stream, const uint8_t* in
     case Mode::kManyKey: {
       const size_t kb = j.n_keys * 16, rkb = j.n_keys * 176;
       GAES_CK(launch_many_key(j.dec, in, out, nblk, j.first + r0, j.bpk, compact,
-                              c->d_mk + kb + (j.dec ? rkb : 0), j.mk_ivs ? c->d_mk + kb + 2 * rkb : nullptr, c->sms,
+                              lane->d_mk + kb + (j.dec ? rkb : 0), j.mk_ivs ? lane->d_mk + kb + 2 * rkb : nullptr, c->sms,
                               stream, tin));
       note_kernel(j.dec ? "k_many_key_dec" : "k_many_key_enc");
       break;
     }
     case Mode::kGeneric: {
-      uint8_t* sc = c->d_scratch;
+      uint8_t* sc = lane->d_scratch;
       GAES_CK(launch_generic(j.dec, in, ivs, rows, j.m, sc + 256 + 4096 + 16, sc, sc + 256, sc + 256 + 4096,
                              out, c->sms, stream));
       note_kernel("k_generic_cbc");
@@ -637,9 +662,28 @@ bool stage_and_check_iv(uint8_t* dst, const uint8_t* src, size_t m, const uint8_
 }
 
 // Runs rows [0, j.n) of `j` on device context c (one shard).
+// Locks the first free lane of c (lane 0 for a lone caller, so its staging
+// buffers -- allocated on first use, cudaMallocHost costs milliseconds -- are
+// reused call after call; lanes 1.. only for concurrent callers); if all
+// are busy, waits on one chosen by thread.
+std::unique_lock<std::mutex> lock_lane(DevCtx* c, Lane** out) {
+  static const int lanes = std::max(1, std::min(kLanes, env_int("GAES_LANES", kLanes)));
+  for (int k = 0; k < lanes; k++) {
+    std::unique_lock<std::mutex> lk(c->lanes[k].mu, std::try_to_lock);
+    if (lk.owns_lock()) {
+      *out = &c->lanes[k];
+      return lk;
+    }
+  }
+  const size_t k = std::hash<std::thread::id>{}(std::this_thread::get_id()) % lanes;
+  *out = &c->lanes[k];
+  return std::unique_lock<std::mutex>(c->lanes[k].mu);
+}
+
 int run_job(DevCtx* c, const Job& j) {
   if (j.n == 0) return GAES_OK;
-  std::lock_guard<std::mutex> lk(c->mu);
+  Lane* lane = nullptr;
+  std::unique_lock<std::mutex> lk = lock_lane(c, &lane);
   int prev = 0;
   GAES_CK(cudaGetDevice(&prev));
   DeviceGuard guard(prev);
@@ -647,17 +691,17 @@ int run_job(DevCtx* c, const Job& j) {
   // On any early return: wait for whatever was issued and drop pending
   // copy-outs, so the next call never writes into this call's buffers.
   struct Drain {
-    DevCtx* c;
+    Lane* lane;
     bool armed = true;
     ~Drain() {
       if (!armed) return;
-      for (auto& s : c->slots) {
+      for (auto& s : lane->slots) {
         if (s.stream) cudaStreamSynchronize(s.stream);
         s.pending_dst = nullptr;
         s.pending_bytes = 0;
       }
     }
-  } drain{c};
+  } drain{lane};
 
   const uint32_t* compact = nullptr;
   if (j.mode != Mode::kGeneric) {
@@ -665,12 +709,12 @@ int run_job(DevCtx* c, const Job& j) {
       compact = j.dec ? c->d_std_dec : c->d_std_enc;
     } else {
       uint32_t* t = nullptr;
-      int rc = tables_for(c, j.box, j.lut, &t);
+      int rc = tables_for(c, lane, lane->slots[0].stream, j.box, j.lut, &t);
       if (rc) return rc;
       compact = t;
     }
   } else {
-    uint8_t* sc = c->d_scratch;
+    uint8_t* sc = lane->d_scratch;
     GAES_CK(cudaMemcpy(sc, j.box, 256, cudaMemcpyHostToDevice));
     GAES_CK(cudaMemcpy(sc + 256, j.lut, 4096, cudaMemcpyHostToDevice));
     GAES_CK(cudaMemcpy(sc + 256 + 4096, j.perm, 16, cudaMemcpyHostToDevice));
@@ -681,21 +725,21 @@ int run_job(DevCtx* c, const Job& j) {
     // keys (and per-key IVs) to the device, batched key schedule there
     // layout: keys (K x 16) | rk_enc (K x 176) | rk_dec (K x 176) | ivs (K x 16)
     const size_t need = j.n_keys * (16 + 176 + 176 + 16);
-    if (c->mk_cap < need) {
-      if (c->d_mk) cudaFree(c->d_mk);
-      c->d_mk = nullptr;
-      c->mk_cap = 0;
-      GAES_CK(cudaMalloc(&c->d_mk, need));
-      c->mk_cap = need;
+    if (lane->mk_cap < need) {
+      if (lane->d_mk) cudaFree(lane->d_mk);
+      lane->d_mk = nullptr;
+      lane->mk_cap = 0;
+      GAES_CK(cudaMalloc(&lane->d_mk, need));
+      lane->mk_cap = need;
     }
     const size_t kb = j.n_keys * 16;
-    cudaStream_t s0 = c->slots[0].stream;
-    GAES_CK(cudaMemcpyAsync(c->d_mk, j.mk_keys, kb, cudaMemcpyHostToDevice, s0));
+    cudaStream_t s0 = lane->slots[0].stream;
+    GAES_CK(cudaMemcpyAsync(lane->d_mk, j.mk_keys, kb, cudaMemcpyHostToDevice, s0));
     if (j.mk_ivs)
-      GAES_CK(cudaMemcpyAsync(c->d_mk + kb + 2 * j.n_keys * 176, j.mk_ivs, kb, cudaMemcpyHostToDevice, s0));
+      GAES_CK(cudaMemcpyAsync(lane->d_mk + kb + 2 * j.n_keys * 176, j.mk_ivs, kb, cudaMemcpyHostToDevice, s0));
     // encrypt and equivalent-inverse-cipher (decrypt) schedules
-    GAES_CK(launch_expand_keys(c->d_mk, j.n_keys, c->d_std_enc, c->d_mk + kb,
-                               j.dec ? c->d_mk + kb + j.n_keys * 176 : nullptr, s0));
+    GAES_CK(launch_expand_keys(lane->d_mk, j.n_keys, c->d_std_enc, lane->d_mk + kb,
+                               j.dec ? lane->d_mk + kb + j.n_keys * 176 : nullptr, s0));
     note_kernel("k_expand_keys");
     GAES_CK(cudaStreamSynchronize(s0));
   }
@@ -721,8 +765,8 @@ int run_job(DevCtx* c, const Job& j) {
     uint8_t* dout = const_cast<uint8_t*>(host_dev_view(j.out));
     const uint8_t* div = need_iv ? host_dev_view(j.ivs) : nullptr;
     if (din && dout && (!need_iv || div)) {
-      cudaStream_t st = c->slots[0].stream;
-      int rc = launch_chunk(c, j, st, din, dout, div, 0, j.n, compact, 0);
+      cudaStream_t st = lane->slots[0].stream;
+      int rc = launch_chunk(c, lane, j, st, din, dout, div, 0, j.n, compact, 0);
       if (rc) return rc;
       GAES_CK(cudaStreamSynchronize(st));
       drain.armed = false;
@@ -757,12 +801,12 @@ int run_job(DevCtx* c, const Job& j) {
   const size_t nchunks = chunks.size();
   const int used_slots = (int)std::min<size_t>(kSlots, nchunks);
   for (int k = 0; k < used_slots; k++) {
-    int rc = ensure_slot(c->slots[k], max_rows * j.m, need_iv ? max_rows * 16 : 0, !in_pinned, !out_pinned);
+    int rc = ensure_slot(lane->slots[k], max_rows * j.m, need_iv ? max_rows * 16 : 0, !in_pinned, !out_pinned);
     if (rc) return rc;
   }
   int rc_final = GAES_OK;
   for (size_t ci = 0; ci < nchunks; ci++) {
-    Slot& s = c->slots[ci % kSlots];
+    Slot& s = lane->slots[ci % kSlots];
     if (ci >= (size_t)kSlots) {
       int rc = finish_slot(s);
       if (rc) return rc;
@@ -798,7 +842,7 @@ int run_job(DevCtx* c, const Job& j) {
       GAES_CK(cudaMemcpyAsync(s.d_iv, ivsrc, rows * 16, cudaMemcpyHostToDevice, s.stream));
     }
     const bool iv_tex = jc->ivs && jc->mode == Mode::kChain && j.m == 16;
-    int rc = launch_chunk(c, *jc, s.stream, s.d_in, s.d_out, s.d_iv, r0, rows, compact,
+    int rc = launch_chunk(c, lane, *jc, s.stream, s.d_in, s.d_out, s.d_iv, r0, rows, compact,
                           tex_for(c, s.d_in, s.cap, s.stream),
                           iv_tex ? tex_for(c, s.d_iv, s.iv_cap, s.stream) : TexLease());
     if (rc) return rc;
@@ -813,7 +857,7 @@ int run_job(DevCtx* c, const Job& j) {
   }
   // drain in issue order
   for (size_t ci = (nchunks > (size_t)kSlots ? nchunks - kSlots : 0); ci < nchunks; ci++) {
-    int rc = finish_slot(c->slots[ci % kSlots]);
+    int rc = finish_slot(lane->slots[ci % kSlots]);
     if (rc && !rc_final) rc_final = rc;
   }
   drain.armed = rc_final != GAES_OK;

@@ -67,9 +67,13 @@ class HostPool {
     cv_.notify_all();
     for (auto& w : workers_) w.join();
   }
-  // Runs fn(i) for i in [0, parts) on the workers plus the calling thread.
-  void run(size_t parts, const std::function<void(size_t)>& fn) {
-    std::unique_lock<std::mutex> call(call_mu_);  // one parallel region at a time
+  // Runs fn(i) for i in [0, parts) on the workers plus the calling thread
+  // and returns true -- or returns false at once if another caller's region
+  // is running (concurrent host-API calls then copy on their own threads
+  // instead of queueing for the pool).
+  bool try_run(size_t parts, const std::function<void(size_t)>& fn) {
+    std::unique_lock<std::mutex> call(call_mu_, std::try_to_lock);  // one parallel region at a time
+    if (!call.owns_lock()) return false;
     {
       std::lock_guard<std::mutex> lk(mu_);
       fn_ = &fn;
@@ -83,6 +87,7 @@ class HostPool {
     std::unique_lock<std::mutex> lk(mu_);
     done_cv_.wait(lk, [this] { return pending_ == 0; });
     fn_ = nullptr;
+    return true;
   }
   // Wakes sleeping workers into their spin window (no work).
   void warm() {
@@ -157,7 +162,7 @@ void parallel_ranges(size_t n, size_t min_per_thread, F&& fn) {
     const size_t lo = t * step, hi = std::min(n, lo + step);
     if (lo < hi) fn(lo, hi);
   };
-  host_pool().run(want, part);
+  if (!host_pool().try_run(want, part)) fn(0, n);
 }
 
 inline void par_memcpy(void* dst, const void* src, size_t bytes) {
