@@ -913,3 +913,49 @@ def test_dropin_mixed_shared_and_per_row_iv_chunks(oracle, m):
     back = np.empty_like(data)
     backend_cuda.cbc_decrypt(out, ivs, *oracle.decrypt_tables(key), back)
     assert np.array_equal(back, data)
+
+
+def test_concurrent_host_calls_of_different_kinds_use_separate_lanes(oracle):
+    """Host calls from several threads run on separate per-device lanes with
+    their own scratch: generic (non-standard) tables, many-key schedules,
+    per-row-IV decrypt and shared-IV encrypt at the same time, repeatedly,
+    all bit-exact."""
+    rng = np.random.default_rng(404)
+    key = rng.bytes(16)
+    t = oracle.encrypt_tables(key)
+    perm = np.ascontiguousarray(np.roll(t[3], 3))
+    n = 20000
+    p = rng.integers(0, 256, (n, 32), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    keys = rng.integers(0, 256, (8, 16), dtype=np.uint8)
+    p16 = rng.integers(0, 256, (8 * 5000, 16), dtype=np.uint8)
+    want_generic = np.empty_like(p)
+    backend_cuda.cbc_encrypt(p, ivs, t[0], t[1], t[2], perm, want_generic)
+    want_mk = backend_cuda.many_key_encrypt(p16, keys)
+    want_enc = oracle.encrypt(key, ivs, p, threads=4)
+    errors = []
+
+    def generic():
+        out = np.empty_like(p)
+        backend_cuda.cbc_encrypt(p, ivs, t[0], t[1], t[2], perm, out)
+        return np.array_equal(out, want_generic)
+
+    def many_key():
+        return np.array_equal(backend_cuda.many_key_encrypt(p16, keys), want_mk)
+
+    def chain():
+        out = np.empty_like(p)
+        backend_cuda.cbc_encrypt(p, ivs, *t, out)
+        back = np.empty_like(p)
+        backend_cuda.cbc_decrypt(out, ivs, *oracle.decrypt_tables(key), back)
+        return np.array_equal(out, want_enc) and np.array_equal(back, p)
+
+    def work(fn, k):
+        for _ in range(6):
+            if not fn():
+                errors.append(k)
+
+    th = [threading.Thread(target=work, args=(fn, k)) for k, fn in enumerate((generic, many_key, chain, generic, chain))]
+    [x.start() for x in th]
+    [x.join() for x in th]
+    assert not errors, errors
