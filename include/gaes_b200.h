@@ -143,7 +143,9 @@ GAES_API int gaes_many_key_decrypt(const uint8_t *data, size_t blocks_per_key, s
  * `out` may equal `in` or overlap it: where a kernel would read a block
  * another thread may already have overwritten (CBC decrypt of multi-block
  * rows in place, any partial overlap) the input is first copied to a
- * private stream-ordered buffer. */
+ * private stream-ordered buffer.  All of them are capturable into a CUDA
+ * graph (no host synchronisation; captured launches read their input with
+ * plain loads instead of a cached texture object). */
 
 /* n_blocks independent 16-byte rows: out_i = E_K(in_i ^ iv)   (M = 16). */
 GAES_API int gaes_encrypt_blocks_dev(const void *in, void *out, size_t n_blocks,

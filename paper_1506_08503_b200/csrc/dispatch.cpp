@@ -362,6 +362,14 @@ class TexLease {
 TexLease tex_for(DevCtx* c, const void* ptr, size_t bytes, cudaStream_t stream) {
   static const bool enabled = env_int("GAES_TEXIN", 1) != 0;
   if (!enabled || !ptr || bytes < 16) return {};
+  // A launch captured into a CUDA graph may be replayed long after this
+  // cache evicted (destroyed) the texture object; captured launches use LDG.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) {
+    cudaGetLastError();
+    return {};
+  }
+  if (cap != cudaStreamCaptureStatusNone) return {};
   std::lock_guard<std::mutex> lk(c->tex_mu);
   query_tex_limits(c);
   if (c->tex_align < 0 || reinterpret_cast<uintptr_t>(ptr) % (uintptr_t)c->tex_align != 0) return {};
