@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -109,7 +110,8 @@ template <int ILP, bool DEC, int IVM, bool TEXIN = false>
 __global__ void __launch_bounds__(kBlockThreads, 1)
     k_blocks(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks,
              const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
-             const uint4* __restrict__ ivs, uint64_t bpr, cudaTextureObject_t tin, cudaTextureObject_t tiv) {
+             const uint4* __restrict__ ivs, uint64_t bpr, cudaTextureObject_t tin, cudaTextureObject_t tiv,
+             int early) {
   extern __shared__ __align__(1024) char smem[];
   // Warp-interleaved block map: warp w of CTA c owns the 32 consecutive
   // blocks starting at 32 (w * gridDim + c), so a batch smaller than the
@@ -117,16 +119,31 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
   // last grid-stride pass of a large batch is shared by all SMs).  A CTA
   // with no block at all exits before its table fill.
   if ((uint64_t)blockIdx.x * 32 >= n_blocks) return;
-  pdl_prologue(smem, compact);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lb = lane * 4;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
   uint64_t b = ((uint64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x) * 32 + lane;
 
+  // early (single-pass batches): wait for the previous grid first, then put
+  // the input loads in flight before the table fill so their DRAM latency
+  // hides behind it; otherwise fill while the previous grid drains (PDL).
   uint4 cur[ILP];
+  if (early) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
 #pragma unroll
   for (int k = 0; k < ILP; k++)
-    if (b + k * T < n_blocks) cur[k] = TEXIN ? tex1Dfetch<uint4>(tin, (int)(b + k * T)) : ld_stream(in + b + k * T);
+    if (early && b + k * T < n_blocks)
+      cur[k] = TEXIN ? tex1Dfetch<uint4>(tin, (int)(b + k * T)) : ld_stream(in + b + k * T);
+  if (early)
+    fill_tables(smem, compact);
+  else
+    pdl_prologue(smem, compact);
+#pragma unroll
+  for (int k = 0; k < ILP; k++)
+    if (!early && b + k * T < n_blocks)
+      cur[k] = TEXIN ? tex1Dfetch<uint4>(tin, (int)(b + k * T)) : ld_stream(in + b + k * T);
 
   // CHAIN mode: (row, j) of every slot is tracked incrementally -- one
   // 64-bit division per thread instead of one per block.
@@ -597,8 +614,13 @@ static cudaError_t launch_blocks_t(const void* in, void* out, uint64_t n, const 
   if (e != cudaSuccess) return e;
   // every SM that gets at least one warp's 32 blocks (see k_blocks' map)
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(sms, (n + 31) / 32));
+  static const int early_mode = [] {
+    const char* e = std::getenv("GAES_EARLY");
+    return (e && *e) ? std::atoi(e) : 2;  // 0 never, 1 always, 2 single-pass batches
+  }();
+  const int early = early_mode == 1 || (early_mode == 2 && n <= (uint64_t)grid * kBlockThreads * ILP);
   return launch_pdl(kern, grid, kBlockThreads, kSmemBytes, s, (const uint4*)in, (uint4*)out, n, compact, rk,
-                    (const uint4*)ivs, bpr, tin, tiv);
+                    (const uint4*)ivs, bpr, tin, tiv, early);
 }
 
 cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* out, uint64_t n_blocks,
