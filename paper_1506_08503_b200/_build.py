@@ -1,7 +1,8 @@
 """Build libgaes_b200.so in-tree with nvcc for sm_100a (no JIT, no torch ext).
 
 The shared library is the product: CUDA kernels (csrc/kernels.cu) plus the
-C-ABI host dispatcher (csrc/dispatch.cpp), statically linked against cudart
+C-ABI host runtime (csrc/abi.cpp, host_pipeline.cpp, device_ctx.cpp,
+runtime.cpp), statically linked against cudart
 so it loads without torch and ships to the GPU box inside the repo snapshot.
 """
 
@@ -15,10 +16,11 @@ PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG_DIR)
 CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_PATH = os.path.join(PKG_DIR, "libgaes_b200.so")
-SOURCES = ["kernels.cu", "dispatch.cpp"]
-HEADERS = ["gf.cuh", "aes_ttable.cuh", "aes_bitslice.cuh", "kernels.h", "types.h", "host_pool.h", "round_keys.h"]
+SOURCES = ["kernels.cu", "runtime.cpp", "device_ctx.cpp", "host_pipeline.cpp", "abi.cpp"]
+HEADERS = ["gf.cuh", "aes_ttable.cuh", "aes_bitslice.cuh", "kernels.h", "types.h", "host_pool.h", "round_keys.h",
+           "runtime.h", "device_ctx.h", "host_pipeline.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden",
                      "-Xptxas", "-O3", "-I", os.path.join(REPO, "include")]
 
 

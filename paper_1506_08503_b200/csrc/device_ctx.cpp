@@ -1,0 +1,314 @@
+// device_ctx.cpp -- see device_ctx.h.
+#include "device_ctx.h"
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "aes_bitslice.cuh"
+#include "gf.cuh"
+
+namespace gaes {
+namespace rt {
+
+std::mutex g_ctx_mu;
+// Contexts live for the process (never destroyed, see ~DevCtx).
+std::vector<DevCtx*>& g_ctx = *new std::vector<DevCtx*>();
+int g_ndev = -1;
+
+// Logical device i -> physical CUDA device g_phys[i].  Identity unless
+// GAES_DEVICE_MAP="a,b,..." is set (e.g. "0,0" runs the multi-GPU shard path
+// as two contexts on one GPU -- used to test the sharding on a 1-GPU box; the
+// shards never wait on each other, so sharing a GPU is safe).
+std::vector<int>& g_phys = *new std::vector<int>();
+
+int device_count() {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if (g_ndev < 0) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    g_phys.clear();
+    const char* map = std::getenv("GAES_DEVICE_MAP");
+    if (n > 0 && map && *map) {
+      for (const char* p = map; *p;) {
+        char* end = nullptr;
+        const long d = std::strtol(p, &end, 10);
+        if (end == p) break;
+        if (d >= 0 && d < n) g_phys.push_back((int)d);
+        p = (*end == ',') ? end + 1 : end;
+        if (*end != ',' && *end) break;
+      }
+    }
+    if (g_phys.empty())
+      for (int i = 0; i < n; i++) g_phys.push_back(i);
+    g_ndev = (int)g_phys.size();
+    g_ctx.resize(g_ndev);
+  }
+  return g_ndev;
+}
+
+// Creates the context on first use: GF-layer tables built on the device.
+int get_ctx(int dev, DevCtx** out) {
+  const int n = device_count();
+  if (n <= 0) return fail(GAES_ENODEV, "no CUDA device visible");
+  if (dev < 0 || dev >= n) return fail(GAES_EINVAL, "device index out of range");
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if (g_ctx[dev]) {
+    *out = g_ctx[dev];
+    return GAES_OK;
+  }
+  auto c = std::make_unique<DevCtx>();
+  c->dev = g_phys[dev];
+  int prev = 0;
+  GAES_CK(cudaGetDevice(&prev));
+  DeviceGuard guard(prev);
+  GAES_CK(cudaSetDevice(c->dev));
+  GAES_CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->dev));
+  GAES_CK(cudaMalloc(&c->d_std_enc, kCompactWords * 4));
+  GAES_CK(cudaMalloc(&c->d_std_dec, kCompactWords * 4));
+  GAES_CK(cudaMalloc(&c->d_tmp, 512 + sizeof(int)));
+  uint8_t* d_box = c->d_tmp;
+  int* d_err = reinterpret_cast<int*>(c->d_tmp + 512);
+  GAES_CK(cudaMemset(d_err, 0, sizeof(int)));
+  GAES_CK(launch_gf_build(c->d_std_enc, c->d_std_dec, d_box, d_box + 256, d_err, 0));
+  note_kernel("k_gf_build");
+  int err = 0;
+  GAES_CK(cudaMemcpy(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  GAES_CK(cudaMemcpy(c->std_sbox, d_box, 256, cudaMemcpyDeviceToHost));
+  GAES_CK(cudaMemcpy(c->std_inv, d_box + 256, 256, cudaMemcpyDeviceToHost));
+  uint32_t tmp[kCompactWords];
+  GAES_CK(cudaMemcpy(tmp, c->d_std_enc, sizeof(tmp), cudaMemcpyDeviceToHost));
+  std::memcpy(c->std_te, tmp, sizeof(c->std_te));
+  GAES_CK(cudaMemcpy(tmp, c->d_std_dec, sizeof(tmp), cudaMemcpyDeviceToHost));
+  std::memcpy(c->std_td, tmp, sizeof(c->std_td));
+  for (auto& L : c->lanes) {
+    GAES_CK(cudaMalloc(&L.d_scratch, 256 + 4096 + 16 + 176 + 512));
+    for (auto& s : L.slots) {
+      GAES_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+      GAES_CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    }
+  }
+  if (err) return fail(GAES_ETABLE, "GF layer self check failed (S^-1 o S != id or M.M^-1 != I)");
+  // The device-built S-box must equal the host restatement of the same
+  // field arithmetic (gf.cuh is compiled for both sides).
+  for (int v = 0; v < 256; v++)
+    if (c->std_sbox[v] != sbox_forward((uint8_t)v) || c->std_inv[v] != sbox_inverse((uint8_t)v))
+      return fail(GAES_ETABLE, "device GF tables disagree with the host field arithmetic");
+  for (int r = 0; r < 4; r++)
+    for (int j = 0; j < 4; j++)
+      for (int x = 0; x < 256; x++) {
+        c->std_mix_fwd[(r * 4 + j) * 256 + x] = gf_mul(mix_coef(false, r, j), (uint8_t)x);
+        c->std_mix_inv[(r * 4 + j) * 256 + x] = gf_mul(mix_coef(true, r, j), (uint8_t)x);
+      }
+  g_ctx[dev] = c.release();
+  *out = g_ctx[dev];
+  return GAES_OK;
+}
+
+// True if the caller's tables equal the device GF layer's (the usual drop-in
+// case: aes_cbc._encrypt_tables / _decrypt_tables build exactly these).
+bool is_standard(const DevCtx* c, bool dec, const uint8_t* box, const uint8_t* lut, const uint8_t* perm) {
+  static const uint8_t kShift[16] = {0, 5, 10, 15, 4, 9, 14, 3, 8, 13, 2, 7, 12, 1, 6, 11};
+  static const uint8_t kInvShift[16] = {0, 13, 10, 7, 4, 1, 14, 11, 8, 5, 2, 15, 12, 9, 6, 3};
+  return std::memcmp(box, dec ? c->std_inv : c->std_sbox, 256) == 0 &&
+         std::memcmp(lut, dec ? c->std_mix_inv : c->std_mix_fwd, 4096) == 0 &&
+         std::memcmp(perm, dec ? kInvShift : kShift, 16) == 0;
+}
+
+// Context of the caller's current CUDA device (first logical device mapped
+// to it).
+int current_ctx(DevCtx** out) {
+  int dev = 0;
+  if (device_count() <= 0) return fail(GAES_ENODEV, "no CUDA device visible");
+  GAES_CK(cudaGetDevice(&dev));
+  for (size_t i = 0; i < g_phys.size(); i++)
+    if (g_phys[i] == dev) return get_ctx((int)i, out);
+  return fail(GAES_EINVAL, "current device is not in GAES_DEVICE_MAP");
+}
+
+// Compact T tables for caller-supplied (box, lut), cached per device (up to
+// 64 sets, never evicted: a concurrent job may be about to launch with any
+// cached pointer).  Past that, the tables are built into the lane's own
+// buffer for this job.  `stream` is the lane's stream.
+int tables_for(DevCtx* c, Lane* lane, cudaStream_t stream, const uint8_t* box, const uint8_t* lut,
+               uint32_t** out) {
+  std::string key(reinterpret_cast<const char*>(box), 256);
+  key.append(reinterpret_cast<const char*>(lut), 4096);
+  std::lock_guard<std::mutex> lk(c->cache_mu);
+  auto it = c->cache.find(key);
+  if (it != c->cache.end()) {
+    *out = it->second;
+    return GAES_OK;
+  }
+  const bool cache_it = c->cache.size() < 64;
+  struct DevBuf {  // freed on every exit path unless released
+    void* p = nullptr;
+    ~DevBuf() {
+      if (p) cudaFree(p);
+    }
+  } d, d_in;
+  uint32_t* tables = nullptr;
+  if (cache_it) {
+    GAES_CK(cudaMalloc(&d.p, kCompactWords * 4));
+    tables = static_cast<uint32_t*>(d.p);
+  } else {
+    if (!lane->d_tables) GAES_CK(cudaMalloc(&lane->d_tables, kCompactWords * 4));
+    tables = lane->d_tables;
+  }
+  GAES_CK(cudaMalloc(&d_in.p, 256 + 4096));
+  uint8_t* in8 = static_cast<uint8_t*>(d_in.p);
+  GAES_CK(cudaMemcpyAsync(in8, box, 256, cudaMemcpyHostToDevice, stream));
+  GAES_CK(cudaMemcpyAsync(in8 + 256, lut, 4096, cudaMemcpyHostToDevice, stream));
+  GAES_CK(launch_build_tables(in8, in8 + 256, tables, stream));
+  note_kernel("k_build_tables");
+  GAES_CK(cudaStreamSynchronize(stream));
+  if (cache_it) {
+    d.p = nullptr;
+    c->cache.emplace(key, tables);
+  }
+  *out = tables;
+  return GAES_OK;
+}
+
+// Texture limits of c->dev, queried once.  Must be called with c->tex_mu held.
+void query_tex_limits(DevCtx* c) {
+  if (c->tex_align != 0) return;
+  int align = 0, maxw = 0;
+  if (cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, c->dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxTexture1DLinearWidth, c->dev) != cudaSuccess) {
+    cudaGetLastError();
+    c->tex_align = -1;
+  } else {
+    c->tex_align = std::max(align, 16);
+    c->tex_max_texels = (size_t)maxw;
+  }
+}
+
+
+// A linear uint4 texture over [ptr, ptr + bytes) for the texture-path input
+// loads, cached per device by pointer (callers and the staging slots reuse
+// buffers).  Empty (handle 0) when disabled (GAES_TEXIN=0), misaligned, too
+// large or unavailable -- the kernels then use LDG.  Must be called with
+// c->dev current and the lease used for one launch on `stream`.  At 64
+// entries the least recently used idle entry is evicted after waiting for
+// the launches that read it (its `last` event); entries lent out right now
+// are never evicted.
+TexLease tex_for(DevCtx* c, const void* ptr, size_t bytes, cudaStream_t stream) {
+  static const bool enabled = env_int("GAES_TEXIN", 1) != 0;
+  if (!enabled || !ptr || bytes < 16) return {};
+  // A launch captured into a CUDA graph may be replayed long after this
+  // cache evicted (destroyed) the texture object; captured launches use LDG.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) {
+    cudaGetLastError();
+    return {};
+  }
+  if (cap != cudaStreamCaptureStatusNone) return {};
+  std::lock_guard<std::mutex> lk(c->tex_mu);
+  query_tex_limits(c);
+  if (c->tex_align < 0 || reinterpret_cast<uintptr_t>(ptr) % (uintptr_t)c->tex_align != 0) return {};
+  if (bytes / 16 > c->tex_max_texels || bytes / 16 > 0x7FFFFFFFull) return {};
+  for (auto& t : c->tex_cache)
+    if (t->ptr == ptr && t->bytes >= bytes) {
+      t->users.fetch_add(1, std::memory_order_acquire);
+      t->stamp = ++c->tex_clock;
+      return TexLease(t.get(), stream);
+    }
+  if (c->tex_cache.size() >= 64) {
+    // users only grows under tex_mu, so an idle entry seen here stays idle
+    size_t victim = c->tex_cache.size();
+    for (size_t i = 0; i < c->tex_cache.size(); i++)
+      if (c->tex_cache[i]->users.load(std::memory_order_acquire) == 0 &&
+          (victim == c->tex_cache.size() || c->tex_cache[i]->stamp < c->tex_cache[victim]->stamp))
+        victim = i;
+    if (victim == c->tex_cache.size()) return {};
+    auto& v = c->tex_cache[victim];
+    if (cudaEventSynchronize(v->last) != cudaSuccess) {
+      cudaGetLastError();
+      return {};
+    }
+    cudaDestroyTextureObject(v->tex);
+    cudaEventDestroy(v->last);
+    c->tex_cache.erase(c->tex_cache.begin() + victim);
+  }
+  auto e = std::make_unique<DevCtx::Tex>();
+  if (cudaEventCreateWithFlags(&e->last, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return {};
+  }
+  cudaResourceDesc rd = {};
+  rd.resType = cudaResourceTypeLinear;
+  rd.res.linear.devPtr = const_cast<void*>(ptr);
+  rd.res.linear.desc = cudaCreateChannelDesc<uint4>();
+  rd.res.linear.sizeInBytes = bytes / 16 * 16;
+  cudaTextureDesc td = {};
+  td.readMode = cudaReadModeElementType;
+  if (cudaCreateTextureObject(&e->tex, &rd, &td, nullptr) != cudaSuccess) {
+    cudaGetLastError();
+    cudaEventDestroy(e->last);
+    return {};
+  }
+  e->ptr = ptr;
+  e->bytes = bytes;
+  e->stamp = ++c->tex_clock;
+  e->users.store(1, std::memory_order_relaxed);
+  c->tex_cache.push_back(std::move(e));
+  return TexLease(c->tex_cache.back().get(), stream);
+}
+
+// Largest launch (in 16-byte blocks) that a texture can cover on this
+// device; device-API calls above it are cut into segments so every segment
+// keeps the texture-path loads.  0 = textures unavailable.
+size_t tex_segment_blocks(DevCtx* c) {
+  std::lock_guard<std::mutex> lk(c->tex_mu);
+  query_tex_limits(c);
+  if (c->tex_align < 0) return 0;
+  size_t seg = std::min<size_t>(c->tex_max_texels, 0x7FFFFFFFull);
+  return seg & ~((size_t)(1 << 20) - 1);
+}
+
+// Device-API aliasing.  Every kernel reads a block before writing the same
+// block, so out == in is safe -- except block-parallel CBC decrypt, where the
+// first lane of each warp reads its chain value in[b-1] from a block another
+// warp may already have overwritten.  Partially overlapping ranges are unsafe
+// for every kernel.  In those cases the input is first copied to a
+// stream-ordered private buffer (freed on the same stream after the launch).
+
+int private_input_if_aliased(const void* in, const void* out, size_t bytes, bool identical_is_unsafe,
+                             cudaStream_t stream, const void** src, PrivateInput* tmp) {
+  *src = in;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(in), b = reinterpret_cast<uintptr_t>(out);
+  const bool overlap = a < b + bytes && b < a + bytes;
+  if (!overlap || (a == b && !identical_is_unsafe)) return GAES_OK;
+  GAES_CK(cudaMallocAsync(&tmp->ptr, bytes, stream));
+  tmp->stream = stream;
+  GAES_CK(cudaMemcpyAsync(tmp->ptr, in, bytes, cudaMemcpyDeviceToDevice, stream));
+  *src = tmp->ptr;
+  return GAES_OK;
+}
+
+
+
+int ilp_default() {
+  // ILP 1 measured ~1% faster than 2 at configs 2 and 3 (finer tail, 40 regs)
+  static int ilp = std::max(1, std::min(2, env_int("GAES_ILP", 1)));
+  return ilp;
+}
+
+cudaError_t launch_enc_folded(DevCtx* c, const void* in, void* out, uint64_t n, const uint32_t* compact,
+                              const RoundKeys& k, int ilp, cudaStream_t s, cudaTextureObject_t tin) {
+  if (g_variant.load() == 2) {
+    static thread_local BitsliceKeys bk;
+    bs_make_keys(k.w, bk);
+    note_kernel("k_bs_blocks");
+    return launch_bs_blocks(in, out, n, bk, c->sms, s);
+  }
+  note_kernel("k_blocks_enc_folded");
+  return launch_blocks(false, kIvFolded, ilp, in, out, n, compact, k, nullptr, 1, c->sms, s, tin);
+}
+
+}  // namespace rt
+}  // namespace gaes

@@ -1,6 +1,4 @@
-for e in 0 2 0 2; do
-echo "GAES_EARLY=$e"
-GAES_EARLY=$e python scripts/exp/small_graph_probe.py 2>&1 | grep -E "2\^(14|16|18)"
-GAES_EARLY=$e python bench.py --config 1 --no-cpu-baseline --no-e2e > gpurun_out/b1.json; python -c "
-import json; d=json.load(open('gpurun_out/b1.json')); print('cfg1', d['value'], d['decrypt_gbs_per_gpu'])"
-done
+python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+python bench.py --no-cpu-baseline > gpurun_out/b2.json; python -c "
+import json; d=json.load(open('gpurun_out/b2.json')); print(d['value'], d['e2e']['value'], d['e2e_dropin']['value'], d['roofline']['frac'], d['gpu_launches'])"
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')"
