@@ -365,8 +365,28 @@ def run_reference_impl(args):
 
 # ----------------------------------------------------------------------------- ours
 
+def _relaunch_under_torchrun(n: int) -> int:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-run this same
+    command as N ranks, one per GPU, over 127.0.0.1 (what the driver does)."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}", file=sys.stderr)
+        return 2
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    import subprocess
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "RANK" not in os.environ:
+        return _relaunch_under_torchrun(args.gpus)
     if args.impl == "reference":
         return run_reference_impl(args)
 
