@@ -298,6 +298,56 @@ def cpu_baseline(key, iv, budget_s: float):
             "logical_cpus": threads, "physical_cores": physical}
 
 
+def reference_api_e2e(key: bytes, iv: bytes, n: int = 1 << 16):
+    """the reference's own public entry point end to end at
+    config 1 -- gaes.encrypt_batch_parallel(key, IVSet.shared(iv), batch) on
+    the unchanged package from baseline/_ref -- with its compiled backend on
+    all host threads, and the same call with this repo's cuda backend
+    registered (drop-in; one worker).  Batch construction is outside the
+    timing.  None when baseline/_ref is absent."""
+    ref_dir = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "gaes")):
+        return None
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    try:
+        import gaes
+        from gaes import parallel
+
+        from paper_1506_08503_b200 import plugin
+    except Exception as e:  # pragma: no cover - informational only
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+    rng = np.random.default_rng(SEED)
+    data = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    batch = gaes.MessageBatch(data=data, original_lens=(16,) * n)
+    ivs = gaes.IVSet.shared(iv)
+    threads = os.cpu_count() or 1
+    prev = gaes.backend.name()
+
+    def timed(workers):
+        parallel.encrypt_batch_parallel(key, ivs, batch, workers)
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            out = parallel.encrypt_batch_parallel(key, ivs, batch, workers)
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts), out
+
+    try:
+        gaes.backend.select("compiled" if "compiled" in gaes.backend.available() else "numpy")
+        kind = gaes.backend.name()
+        t_ref, c_ref = timed(threads)
+        plugin.register(gaes_module=gaes, select=True)
+        t_gpu, c_gpu = timed(1)
+    finally:
+        gaes.backend.select(prev)
+    return {"api": "gaes.encrypt_batch_parallel(key, IVSet.shared(iv), batch) -- config 1, 65536 x 16 B",
+            "reference": {"backend": kind, "workers": threads, "ms": round(t_ref * 1e3, 3),
+                          "gbs": round(n * 16 / t_ref / 1e9, 4)},
+            "cuda_backend": {"workers": 1, "ms": round(t_gpu * 1e3, 3), "gbs": round(n * 16 / t_gpu / 1e9, 4)},
+            "identical_bytes": bool(np.array_equal(c_ref, c_gpu))}
+
+
 def _openssl_worker(args):
     key, iv, n, budget_s, seed = args
     from cryptography.hazmat.primitives.ciphers import Cipher, algorithms, modes
@@ -715,6 +765,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(key, iv, args.cpu_seconds)
         openssl = openssl_rate(key, iv)
+        try:
+            cpu["reference_api_e2e_cfg1"] = reference_api_e2e(key, iv)
+        except Exception as e:  # pragma: no cover - informational only
+            cpu["reference_api_e2e_cfg1"] = {"unavailable": f"{type(e).__name__}: {e}"}
 
     if rank == 0:
         line = {
