@@ -165,7 +165,6 @@ bool stage_and_check_iv(uint8_t* dst, const uint8_t* src, size_t m, const uint8_
   return same.load();
 }
 
-// Runs rows [0, j.n) of `j` on device context c (one shard).
 // Locks the first free lane of c (lane 0 for a lone caller, so its staging
 // buffers -- allocated on first use, cudaMallocHost costs milliseconds -- are
 // reused call after call; lanes 1.. only for concurrent callers); if all
@@ -184,6 +183,7 @@ std::unique_lock<std::mutex> lock_lane(DevCtx* c, Lane** out) {
   return std::unique_lock<std::mutex>(c->lanes[k].mu);
 }
 
+// Runs rows [0, j.n) of `j` on device context c (one shard).
 int run_job(DevCtx* c, const Job& j) {
   if (j.n == 0) return GAES_OK;
   Lane* lane = nullptr;
@@ -286,6 +286,8 @@ int run_job(DevCtx* c, const Job& j) {
   static const size_t pageable_chunk = (size_t)std::max(1, env_int("GAES_PAGEABLE_CHUNK_MB", 16)) << 20;
   const size_t base_bytes = (in_pinned && out_pinned) ? chunk_bytes() : std::min<size_t>(chunk_bytes(), pageable_chunk);
   const size_t base_rows = std::max<size_t>(1, base_bytes / j.m);
+  // (splitting small staged jobs further was measured slower: per-chunk
+  // fixed costs outweigh the copy/transfer overlap below ~2 MiB)
   const size_t min_rows = std::max<size_t>(1, base_rows / 8);
   std::vector<std::pair<size_t, size_t>> chunks;  // (first row, rows)
   {
