@@ -53,6 +53,7 @@ SIGNATURES = {
     "gaes_set_variant": (_i, [_i]),
     "gaes_probe_round_rate": (_i, [_i, ctypes.c_uint32, _vp, _vp]),
     "gaes_probe_lds_peak": (_i, [_i, ctypes.c_uint32, _vp, _vp]),
+    "gaes_uses_sbox_texture": (_i, [_i]),
 }
 
 

@@ -73,9 +73,9 @@ GAES_API int gaes_probe_round_rate(int device, uint32_t iters, double* lookups_p
   const RoundKeys k = make_enc_keys(rk, nullptr, false);
   GAES_CK(cudaEventCreate(&r.a));
   GAES_CK(cudaEventCreate(&r.b));
-  GAES_CK(launch_round_probe(c->d_std_enc, k, 16, r.sink, c->sms, 0));  // warm-up
+  GAES_CK(launch_round_probe(c->d_std_enc, k, 16, r.sink, c->sms, 0, c->tex_s_enc));  // warm-up
   GAES_CK(cudaEventRecord(r.a, 0));
-  GAES_CK(launch_round_probe(c->d_std_enc, k, iters, r.sink, c->sms, 0));
+  GAES_CK(launch_round_probe(c->d_std_enc, k, iters, r.sink, c->sms, 0, c->tex_s_enc));
   GAES_CK(cudaEventRecord(r.b, 0));
   GAES_CK(cudaEventSynchronize(r.b));
   note_kernel("k_round_probe");
@@ -121,6 +121,13 @@ GAES_API int gaes_probe_lds_peak(int device, uint32_t iters, double* lookups_per
   if (lookups_per_sec) *lookups_per_sec = lookups / (t / 1e3);
   if (ms) *ms = t;
   return GAES_OK;
+}
+
+GAES_API int gaes_uses_sbox_texture(int device) {
+  DevCtx* c = nullptr;
+  int rc = get_ctx(device, &c);
+  if (rc) return rc;
+  return c->tex_s_enc && c->tex_s_dec ? 1 : 0;
 }
 
 GAES_API int gaes_gf_tables(int device, uint8_t sbox[256], uint8_t inv_sbox[256], uint32_t te[1024],
@@ -247,7 +254,8 @@ GAES_API int gaes_decrypt_blocks_dev(const void* in, void* out, size_t n_blocks,
   return for_segments(c, n_blocks, [&](size_t off, size_t cnt) {
     const uint4* i = static_cast<const uint4*>(src) + off;
     GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), i, static_cast<uint4*>(out) + off, cnt, c->d_std_dec, k,
-                          nullptr, 1, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream)));
+                          nullptr, 1, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream), 0,
+                          sbox_tex(c, c->d_std_dec)));
     note_kernel("k_blocks_dec_folded");
     return GAES_OK;
   });
@@ -271,7 +279,7 @@ GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m,
   if (bpr == 1) {
     GAES_CK(launch_blocks(false, kIvChain, ilp_default(), src, out, n, c->d_std_enc, k, ivs_dev, 1, c->sms,
                           (cudaStream_t)stream, tex_for(c, src, n * 16, (cudaStream_t)stream),
-                          tex_for(c, ivs_dev, n * 16, (cudaStream_t)stream)));
+                          tex_for(c, ivs_dev, n * 16, (cudaStream_t)stream), sbox_tex(c, c->d_std_enc)));
     note_kernel("k_blocks_enc_chain");
   } else {
     // segments of whole rows, each inside one texture
@@ -283,7 +291,8 @@ GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m,
     for (size_t r = 0; r < n; r += seg_rows) {
       const size_t cnt = std::min(seg_rows, n - r);
       GAES_CK(launch_cbc_enc_rows(i8 + r * m, o8 + r * m, cnt, bpr, c->d_std_enc, k, v8 ? v8 + r * 16 : nullptr,
-                                  c->sms, (cudaStream_t)stream, tex_for(c, i8 + r * m, cnt * m, (cudaStream_t)stream)));
+                                  c->sms, (cudaStream_t)stream, tex_for(c, i8 + r * m, cnt * m, (cudaStream_t)stream),
+                                  sbox_tex(c, c->d_std_enc)));
     }
     note_kernel("k_cbc_enc_rows");
   }
@@ -307,7 +316,8 @@ GAES_API int gaes_cbc_decrypt_dev(const void* in, void* out, size_t n, size_t m,
   if (rc) return rc;
   GAES_CK(launch_blocks(true, kIvChain, ilp_default(), src, out, n * bpr, c->d_std_dec, k, ivs_dev, bpr, c->sms,
                         (cudaStream_t)stream, tex_for(c, src, n * bpr * 16, (cudaStream_t)stream),
-                        bpr == 1 && ivs_dev ? tex_for(c, ivs_dev, n * 16, (cudaStream_t)stream) : TexLease()));
+                        bpr == 1 && ivs_dev ? tex_for(c, ivs_dev, n * 16, (cudaStream_t)stream) : TexLease(),
+                        sbox_tex(c, c->d_std_dec)));
   note_kernel("k_blocks_dec_chain");
   return GAES_OK;
 }
@@ -338,7 +348,8 @@ GAES_API int gaes_many_key_encrypt_dev(const void* in, void* out, size_t blocks_
   return for_segments(c, blocks_per_key * k, [&](size_t off, size_t cnt) {
     const uint4* i = static_cast<const uint4*>(src) + off;
     GAES_CK(launch_many_key(false, i, static_cast<uint4*>(out) + off, cnt, off, blocks_per_key, c->d_std_enc, rk_enc,
-                            ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream)));
+                            ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream),
+                            sbox_tex(c, c->d_std_enc)));
     note_kernel("k_many_key_enc");
     return GAES_OK;
   });
@@ -358,7 +369,8 @@ GAES_API int gaes_many_key_decrypt_dev(const void* in, void* out, size_t blocks_
   return for_segments(c, blocks_per_key * k, [&](size_t off, size_t cnt) {
     const uint4* i = static_cast<const uint4*>(src) + off;
     GAES_CK(launch_many_key(true, i, static_cast<uint4*>(out) + off, cnt, off, blocks_per_key, c->d_std_dec, rk_dec,
-                            ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream)));
+                            ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream),
+                            sbox_tex(c, c->d_std_dec)));
     note_kernel("k_many_key_dec");
     return GAES_OK;
   });

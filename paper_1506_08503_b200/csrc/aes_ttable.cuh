@@ -21,6 +21,7 @@
 // region/table offset for free.
 //     region 0: T0 | T1      region 1: T2 | T3      region 2: S | (unused)
 #pragma once
+#include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "types.h"
@@ -48,11 +49,13 @@ __device__ __forceinline__ uint32_t* stage_word(char* smem, int i) {
 // single L2 round trip per thread), then smem-to-smem replication.  Reading
 // L2 inside the replication loop made every thread wait ~10 dependent L2
 // round trips (~8 us per launch).
-__device__ __forceinline__ void fill_tables(char* smem, const uint32_t* __restrict__ compact) {
+__device__ __forceinline__ void fill_tables(char* smem, const uint32_t* __restrict__ compact, bool with_s = true) {
   for (int i = threadIdx.x; i < kCompactWords; i += blockDim.x) *stage_word(smem, i) = __ldg(compact + i);
   __syncthreads();
-  // 5 tables x 256 entries x 8 uint4 (32 lane copies) per entry
-  for (int q = threadIdx.x; q < 5 * 256 * 8; q += blockDim.x) {
+  // 5 tables x 256 entries x 8 uint4 (32 lane copies) per entry; the S table
+  // (the 5th) only when round 10 reads it from shared memory
+  const int words = (with_s ? 5 : 4) * 256 * 8;
+  for (int q = threadIdx.x; q < words; q += blockDim.x) {
     const int quad = q & 7;
     const int x = (q >> 3) & 255;
     const int tbl = q >> 11;
@@ -63,9 +66,18 @@ __device__ __forceinline__ void fill_tables(char* smem, const uint32_t* __restri
   __syncthreads();
 }
 
-// One full AES-128 encryption of a state already XORed with rk0.
+// S-box byte through the texture path (a 256-byte u8 linear texture: the
+// last round's 16 lookups ride the TEX pipe instead of the saturated L1 /
+// shared data pipe -- profiles/r1_formulation_choice.md).
+__device__ __forceinline__ uint32_t tex_sbox(cudaTextureObject_t t, uint32_t x) {
+  return (uint32_t)tex1Dfetch<unsigned char>(t, (int)x);
+}
+
+// One full AES-128 encryption of a state already XORed with rk0.  tsb: S-box
+// texture for round 10, or 0 to read the replicated S table in smem.
 __device__ __forceinline__ void encrypt_rounds(const char* smem, uint32_t lb, uint32_t& s0, uint32_t& s1,
-                                               uint32_t& s2, uint32_t& s3, const RoundKeys& rk) {
+                                               uint32_t& s2, uint32_t& s3, const RoundKeys& rk,
+                                               cudaTextureObject_t tsb = 0) {
 #pragma unroll
   for (int r = 1; r < 10; r++) {
     const uint32_t t0 = lds_u32(smem, taddr<0>(s0, lb), kOffT0) ^ lds_u32(smem, taddr<1>(s1, lb), kOffT1) ^
@@ -88,17 +100,29 @@ __device__ __forceinline__ void encrypt_rounds(const char* smem, uint32_t lb, ui
 #define GAES_LAST(a, b, c, d)                                                        \
   ((lds_u32(smem, taddr<3>(d, lb), kOffS) * 256u + lds_u32(smem, taddr<2>(c, lb), kOffS)) * 65536u + \
    (lds_u32(smem, taddr<1>(b, lb), kOffS) * 256u + lds_u32(smem, taddr<0>(a, lb), kOffS)))
-  const uint32_t o0 = GAES_LAST(s0, s1, s2, s3) ^ rk.w[40];
-  const uint32_t o1 = GAES_LAST(s1, s2, s3, s0) ^ rk.w[41];
-  const uint32_t o2 = GAES_LAST(s2, s3, s0, s1) ^ rk.w[42];
-  const uint32_t o3 = GAES_LAST(s3, s0, s1, s2) ^ rk.w[43];
+#define GAES_LAST_T(a, b, c, d)                                                                     \
+  ((tex_sbox(tsb, (d) >> 24) * 256u + tex_sbox(tsb, ((c) >> 16) & 0xFF)) * 65536u +                 \
+   (tex_sbox(tsb, ((b) >> 8) & 0xFF) * 256u + tex_sbox(tsb, (a) & 0xFF)))
+  uint32_t o0, o1, o2, o3;
+  if (tsb) {
+    o0 = GAES_LAST_T(s0, s1, s2, s3) ^ rk.w[40];
+    o1 = GAES_LAST_T(s1, s2, s3, s0) ^ rk.w[41];
+    o2 = GAES_LAST_T(s2, s3, s0, s1) ^ rk.w[42];
+    o3 = GAES_LAST_T(s3, s0, s1, s2) ^ rk.w[43];
+  } else {
+    o0 = GAES_LAST(s0, s1, s2, s3) ^ rk.w[40];
+    o1 = GAES_LAST(s1, s2, s3, s0) ^ rk.w[41];
+    o2 = GAES_LAST(s2, s3, s0, s1) ^ rk.w[42];
+    o3 = GAES_LAST(s3, s0, s1, s2) ^ rk.w[43];
+  }
   s0 = o0; s1 = o1; s2 = o2; s3 = o3;
 }
 
 // Equivalent inverse cipher; input state already XORed with rk10; output
 // is InvSub(InvShift(...)) of round 1, NOT yet XORed with rk0.
 __device__ __forceinline__ void decrypt_rounds(const char* smem, uint32_t lb, uint32_t& s0, uint32_t& s1,
-                                               uint32_t& s2, uint32_t& s3, const RoundKeys& rk) {
+                                               uint32_t& s2, uint32_t& s3, const RoundKeys& rk,
+                                               cudaTextureObject_t tsb = 0) {
 #pragma unroll
   for (int r = 9; r >= 1; r--) {
     const uint32_t t0 = lds_u32(smem, taddr<0>(s0, lb), kOffT0) ^ lds_u32(smem, taddr<1>(s3, lb), kOffT1) ^
@@ -115,11 +139,20 @@ __device__ __forceinline__ void decrypt_rounds(const char* smem, uint32_t lb, ui
                         rk.w[4 * r + 3];
     s0 = t0; s1 = t1; s2 = t2; s3 = t3;
   }
-  const uint32_t o0 = GAES_LAST(s0, s3, s2, s1);
-  const uint32_t o1 = GAES_LAST(s1, s0, s3, s2);
-  const uint32_t o2 = GAES_LAST(s2, s1, s0, s3);
-  const uint32_t o3 = GAES_LAST(s3, s2, s1, s0);
+  uint32_t o0, o1, o2, o3;
+  if (tsb) {
+    o0 = GAES_LAST_T(s0, s3, s2, s1);
+    o1 = GAES_LAST_T(s1, s0, s3, s2);
+    o2 = GAES_LAST_T(s2, s1, s0, s3);
+    o3 = GAES_LAST_T(s3, s2, s1, s0);
+  } else {
+    o0 = GAES_LAST(s0, s3, s2, s1);
+    o1 = GAES_LAST(s1, s0, s3, s2);
+    o2 = GAES_LAST(s2, s1, s0, s3);
+    o3 = GAES_LAST(s3, s2, s1, s0);
+  }
 #undef GAES_LAST
+#undef GAES_LAST_T
   s0 = o0; s1 = o1; s2 = o2; s3 = o3;
 }
 

@@ -50,6 +50,29 @@ int device_count() {
   return g_ndev;
 }
 
+// A u8 linear texture over 256 bytes (0 if unavailable).
+cudaTextureObject_t make_byte_texture(const uint8_t* p) {
+  cudaResourceDesc rd = {};
+  rd.resType = cudaResourceTypeLinear;
+  rd.res.linear.devPtr = const_cast<uint8_t*>(p);
+  rd.res.linear.desc = cudaCreateChannelDesc<unsigned char>();
+  rd.res.linear.sizeInBytes = 256;
+  cudaTextureDesc td = {};
+  td.readMode = cudaReadModeElementType;
+  cudaTextureObject_t t = 0;
+  if (cudaCreateTextureObject(&t, &rd, &td, nullptr) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return t;
+}
+
+cudaTextureObject_t sbox_tex(const DevCtx* c, const uint32_t* compact) {
+  if (compact == c->d_std_enc) return c->tex_s_enc;
+  if (compact == c->d_std_dec) return c->tex_s_dec;
+  return 0;
+}
+
 // Creates the context on first use: GF-layer tables built on the device.
 int get_ctx(int dev, DevCtx** out) {
   const int n = device_count();
@@ -90,6 +113,15 @@ int get_ctx(int dev, DevCtx** out) {
       GAES_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
       GAES_CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
     }
+  }
+  // S-box textures for round 10 (standard tables); optional
+  GAES_CK(cudaMalloc(&c->d_sbox, 256));
+  GAES_CK(cudaMalloc(&c->d_inv, 256));
+  GAES_CK(cudaMemcpy(c->d_sbox, d_box, 256, cudaMemcpyDeviceToDevice));
+  GAES_CK(cudaMemcpy(c->d_inv, d_box + 256, 256, cudaMemcpyDeviceToDevice));
+  if (env_int("GAES_TEXS", 1) != 0) {
+    c->tex_s_enc = make_byte_texture(c->d_sbox);
+    c->tex_s_dec = make_byte_texture(c->d_inv);
   }
   if (err) return fail(GAES_ETABLE, "GF layer self check failed (S^-1 o S != id or M.M^-1 != I)");
   // The device-built S-box must equal the host restatement of the same
@@ -306,8 +338,9 @@ cudaError_t launch_enc_folded(DevCtx* c, const void* in, void* out, uint64_t n, 
     note_kernel("k_bs_blocks");
     return launch_bs_blocks(in, out, n, bk, c->sms, s);
   }
-  note_kernel("k_blocks_enc_folded");
-  return launch_blocks(false, kIvFolded, ilp, in, out, n, compact, k, nullptr, 1, c->sms, s, tin);
+  const cudaTextureObject_t tsb = sbox_tex(c, compact);
+  note_kernel(tsb ? "k_blocks_enc_folded+texsbox" : "k_blocks_enc_folded");
+  return launch_blocks(false, kIvFolded, ilp, in, out, n, compact, k, nullptr, 1, c->sms, s, tin, 0, tsb);
 }
 
 }  // namespace rt

@@ -60,6 +60,12 @@ struct DevCtx {
   std::mutex cache_mu;
   std::unordered_map<std::string, uint32_t*> cache;  // (box || lut) -> compact tables; never evicted
   uint8_t* d_tmp = nullptr;      // GF-build outputs + error flag
+  // S-box / inverse S-box bytes (256 B each) and u8 textures over them: the
+  // last round's lookups for the standard tables go through the TEX pipe
+  // (0 = unavailable or GAES_TEXS=0: read the replicated S table in smem)
+  uint8_t* d_sbox = nullptr;
+  uint8_t* d_inv = nullptr;
+  cudaTextureObject_t tex_s_enc = 0, tex_s_dec = 0;
   // linear textures over input buffers (texture-path loads, see k_blocks),
   // least-recently-used first; see tex_for
   struct Tex {
@@ -79,7 +85,9 @@ struct DevCtx {
   // Only runs when initialisation fails (live contexts are never destroyed:
   // freeing after the CUDA runtime has shut down at exit is not allowed).
   ~DevCtx() {
-    for (void* p : {(void*)d_std_enc, (void*)d_std_dec, (void*)d_tmp})
+    for (cudaTextureObject_t t : {tex_s_enc, tex_s_dec})
+      if (t) cudaDestroyTextureObject(t);
+    for (void* p : {(void*)d_std_enc, (void*)d_std_dec, (void*)d_tmp, (void*)d_sbox, (void*)d_inv})
       if (p) cudaFree(p);
     for (auto& L : lanes) {
       for (void* p : {(void*)L.d_scratch, (void*)L.d_mk, (void*)L.d_tables})
@@ -151,6 +159,8 @@ size_t tex_segment_blocks(DevCtx* c);
 int private_input_if_aliased(const void* in, const void* out, size_t bytes, bool identical_is_unsafe,
                              cudaStream_t stream, const void** src, PrivateInput* tmp);
 int ilp_default();
+// S-box texture matching the compact tables `compact` (standard tables only).
+cudaTextureObject_t sbox_tex(const DevCtx* c, const uint32_t* compact);
 // M = 16 shared-IV encrypt: the formulation chosen by measurement
 // (profiles/): T-table unless gaes_set_variant(2) selects the bitsliced kernel.
 cudaError_t launch_enc_folded(DevCtx* c, const void* in, void* out, uint64_t n, const uint32_t* compact,

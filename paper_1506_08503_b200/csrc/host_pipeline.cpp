@@ -95,36 +95,37 @@ int launch_chunk(DevCtx* c, Lane* lane, const Job& j, cudaStream_t stream, const
                  cudaTextureObject_t tiv = 0) {
   const uint64_t bpr = j.m / 16;
   const uint64_t nblk = rows * bpr;
+  const cudaTextureObject_t tsb = sbox_tex(c, compact);
   switch (j.mode) {
     case Mode::kFolded:
       if (j.dec) {
         GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), in, out, nblk, compact, j.rk, nullptr, 1,
-                              c->sms, stream, tin));
+                              c->sms, stream, tin, 0, tsb));
         note_kernel("k_blocks_dec_folded");
       } else if (j.standard || g_variant.load() < 2) {
         GAES_CK(launch_enc_folded(c, in, out, nblk, compact, j.rk, ilp_default(), stream,
                                   tin));
       } else {  // bitsliced kernel has the standard S-box built in; caller tables -> T-table
         GAES_CK(launch_blocks(false, kIvFolded, ilp_default(), in, out, nblk, compact, j.rk, nullptr, 1,
-                              c->sms, stream));
+                              c->sms, stream, 0, 0, tsb));
         note_kernel("k_blocks_enc_folded");
       }
       break;
     case Mode::kChain:
       GAES_CK(launch_blocks(j.dec, kIvChain, ilp_default(), in, out, nblk, compact, j.rk,
-                            j.ivs ? ivs : nullptr, bpr, c->sms, stream, tin, j.ivs ? tiv : 0));
+                            j.ivs ? ivs : nullptr, bpr, c->sms, stream, tin, j.ivs ? tiv : 0, tsb));
       note_kernel(j.dec ? "k_blocks_dec_chain" : "k_blocks_enc_chain");
       break;
     case Mode::kEncRows:
       GAES_CK(launch_cbc_enc_rows(in, out, rows, bpr, compact, j.rk, j.ivs ? ivs : nullptr, c->sms,
-                                  stream, tin));
+                                  stream, tin, tsb));
       note_kernel("k_cbc_enc_rows");
       break;
     case Mode::kManyKey: {
       const size_t kb = j.n_keys * 16, rkb = j.n_keys * 176;
       GAES_CK(launch_many_key(j.dec, in, out, nblk, j.first + r0, j.bpk, compact,
                               lane->d_mk + kb + (j.dec ? rkb : 0), j.mk_ivs ? lane->d_mk + kb + 2 * rkb : nullptr, c->sms,
-                              stream, tin));
+                              stream, tin, tsb));
       note_kernel(j.dec ? "k_many_key_dec" : "k_many_key_enc");
       break;
     }

@@ -80,9 +80,10 @@ __global__ void k_build_tables(const uint8_t* __restrict__ box, const uint8_t* _
 // next launch on the stream to start its CTAs as SMs free up, fill our
 // tables, then wait for the previous launch's memory before any global
 // access to data.  griddepcontrol.* are no-ops without the PDL attribute.
-__device__ __forceinline__ void pdl_prologue(char* smem, const uint32_t* __restrict__ compact) {
+__device__ __forceinline__ void pdl_prologue(char* smem, const uint32_t* __restrict__ compact,
+                                             bool with_s = true) {
   asm volatile("griddepcontrol.launch_dependents;");
-  fill_tables(smem, compact);
+  fill_tables(smem, compact, with_s);
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
     k_blocks(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks,
              const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
              const uint4* __restrict__ ivs, uint64_t bpr, cudaTextureObject_t tin, cudaTextureObject_t tiv,
-             int early) {
+             int early, cudaTextureObject_t tsb) {
   extern __shared__ __align__(1024) char smem[];
   // Warp-interleaved block map: warp w of CTA c owns the 32 consecutive
   // blocks starting at 32 (w * gridDim + c), so a batch smaller than the
@@ -137,9 +138,9 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
     if (early && b + k * T < n_blocks)
       cur[k] = TEXIN ? tex1Dfetch<uint4>(tin, (int)(b + k * T)) : ld_stream(in + b + k * T);
   if (early)
-    fill_tables(smem, compact);
+    fill_tables(smem, compact, tsb == 0);
   else
-    pdl_prologue(smem, compact);
+    pdl_prologue(smem, compact, tsb == 0);
 #pragma unroll
   for (int k = 0; k < ILP; k++)
     if (!early && b + k * T < n_blocks)
@@ -203,10 +204,10 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
         uint32_t s0 = cur[k].x, s1 = cur[k].y, s2 = cur[k].z, s3 = cur[k].w;
         if (!DEC) {
           s0 ^= rk.w[0] ^ x.x; s1 ^= rk.w[1] ^ x.y; s2 ^= rk.w[2] ^ x.z; s3 ^= rk.w[3] ^ x.w;
-          encrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
+          encrypt_rounds(smem, lb, s0, s1, s2, s3, rk, tsb);
         } else {
           s0 ^= rk.w[40]; s1 ^= rk.w[41]; s2 ^= rk.w[42]; s3 ^= rk.w[43];
-          decrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
+          decrypt_rounds(smem, lb, s0, s1, s2, s3, rk, tsb);
           s0 ^= rk.w[0] ^ x.x; s1 ^= rk.w[1] ^ x.y; s2 ^= rk.w[2] ^ x.z; s3 ^= rk.w[3] ^ x.w;
         }
         st_stream(out + bk, make_uint4(s0, s1, s2, s3));
@@ -247,15 +248,15 @@ template <bool PAIRS, bool TEXIN>
 __global__ void __launch_bounds__(kBlockThreads, 1)
     k_cbc_enc_rows(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_rows, uint64_t bpr,
                    const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
-                   const uint4* __restrict__ ivs, cudaTextureObject_t tin) {
+                   const uint4* __restrict__ ivs, cudaTextureObject_t tin, cudaTextureObject_t tsb) {
   extern __shared__ __align__(1024) char smem[];
-  pdl_prologue(smem, compact);
+  pdl_prologue(smem, compact, tsb == 0);
   const uint32_t lb = (threadIdx.x & 31) * 4;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
   auto enc = [&](const uint4& p, uint4& c) {
     uint32_t s0 = p.x ^ c.x ^ rk.w[0], s1 = p.y ^ c.y ^ rk.w[1];
     uint32_t s2 = p.z ^ c.z ^ rk.w[2], s3 = p.w ^ c.w ^ rk.w[3];
-    encrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
+    encrypt_rounds(smem, lb, s0, s1, s2, s3, rk, tsb);
     c = make_uint4(s0, s1, s2, s3);
   };
   auto load = [&](uint64_t i) { return TEXIN ? tex1Dfetch<uint4>(tin, (int)i) : __ldg(in + i); };
@@ -418,9 +419,9 @@ template <bool DEC, bool TEXIN = false>
 __global__ void __launch_bounds__(kManyKeyThreads, 1)
     k_many_key(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks, uint64_t first,
                uint64_t bpk, const uint32_t* __restrict__ compact, const uint4* __restrict__ rks,
-               const uint4* __restrict__ ivs, cudaTextureObject_t tin) {
+               const uint4* __restrict__ ivs, cudaTextureObject_t tin, cudaTextureObject_t tsb) {
   extern __shared__ __align__(1024) char smem[];
-  pdl_prologue(smem, compact);
+  pdl_prologue(smem, compact, tsb == 0);
   const uint32_t lb = (threadIdx.x & 31) * 4;
   // Each CTA owns one contiguous range and its threads stride by blockDim
   // inside it, so a thread crosses into the next key only at real key
@@ -457,10 +458,10 @@ __global__ void __launch_bounds__(kManyKeyThreads, 1)
     uint32_t s0 = cur.x, s1 = cur.y, s2 = cur.z, s3 = cur.w;
     if (!DEC) {
       s0 ^= rk.w[0]; s1 ^= rk.w[1]; s2 ^= rk.w[2]; s3 ^= rk.w[3];
-      encrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
+      encrypt_rounds(smem, lb, s0, s1, s2, s3, rk, tsb);
     } else {
       s0 ^= rk.w[40]; s1 ^= rk.w[41]; s2 ^= rk.w[42]; s3 ^= rk.w[43];
-      decrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
+      decrypt_rounds(smem, lb, s0, s1, s2, s3, rk, tsb);
       s0 ^= rk.w[0]; s1 ^= rk.w[1]; s2 ^= rk.w[2]; s3 ^= rk.w[3];
     }
     st_stream(out + b, make_uint4(s0, s1, s2, s3));
@@ -506,12 +507,12 @@ __global__ void __launch_bounds__(kBsThreads)
 // (reported beside the nominal 32 lanes/clk/SM figure).
 __global__ void __launch_bounds__(kBlockThreads, 1)
     k_round_probe(const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk, uint32_t iters,
-                  uint32_t* __restrict__ sink) {
+                  uint32_t* __restrict__ sink, cudaTextureObject_t tsb) {
   extern __shared__ __align__(1024) char smem[];
-  fill_tables(smem, compact);
+  fill_tables(smem, compact, tsb == 0);
   const uint32_t lb = (threadIdx.x & 31) * 4;
   uint32_t s0 = threadIdx.x, s1 = blockIdx.x, s2 = threadIdx.x * 7, s3 = ~threadIdx.x;
-  for (uint32_t i = 0; i < iters; i++) encrypt_rounds(smem, lb, s0, s1, s2, s3, rk);
+  for (uint32_t i = 0; i < iters; i++) encrypt_rounds(smem, lb, s0, s1, s2, s3, rk, tsb);
   if ((s0 ^ s1 ^ s2 ^ s3) == 0x12345678u) sink[0] = s0;  // keep the work alive
 }
 
@@ -608,7 +609,8 @@ cudaError_t launch_build_tables(const uint8_t* box, const uint8_t* lut, uint32_t
 template <int ILP, bool DEC, int IVM, bool TEXIN = false>
 static cudaError_t launch_blocks_t(const void* in, void* out, uint64_t n, const uint32_t* compact,
                                    const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms, cudaStream_t s,
-                                   cudaTextureObject_t tin = 0, cudaTextureObject_t tiv = 0) {
+                                   cudaTextureObject_t tin = 0, cudaTextureObject_t tiv = 0,
+                                   cudaTextureObject_t tsb = 0) {
   auto kern = k_blocks<ILP, DEC, IVM, TEXIN>;
   cudaError_t e = set_smem(kern);
   if (e != cudaSuccess) return e;
@@ -620,37 +622,38 @@ static cudaError_t launch_blocks_t(const void* in, void* out, uint64_t n, const 
   }();
   const int early = early_mode == 1 || (early_mode == 2 && n <= (uint64_t)grid * kBlockThreads * ILP);
   return launch_pdl(kern, grid, kBlockThreads, kSmemBytes, s, (const uint4*)in, (uint4*)out, n, compact, rk,
-                    (const uint4*)ivs, bpr, tin, tiv, early);
+                    (const uint4*)ivs, bpr, tin, tiv, early, tsb);
 }
 
 cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* out, uint64_t n_blocks,
                           const uint32_t* compact, const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms,
-                          cudaStream_t s, cudaTextureObject_t tin, cudaTextureObject_t tiv) {
+                          cudaStream_t s, cudaTextureObject_t tin, cudaTextureObject_t tiv,
+                          cudaTextureObject_t tsb) {
   if (n_blocks == 0) return cudaSuccess;
   if (ivmode == kIvChain && bpr == 1 && ivs) ivmode = kIvRows;  // per-row IVs, one block per row
   if (n_blocks > 0x7FFFFFFFull) tiv = 0;
   if (ivmode == kIvRows) {
     if (!(tin && n_blocks <= 0x7FFFFFFFull)) tin = 0;
     if (tin) {
-      if (dec) return launch_blocks_t<1, true, kIvRows, true>(in, out, n_blocks, compact, rk, ivs, 1, sms, s, tin, tiv);
-      return launch_blocks_t<1, false, kIvRows, true>(in, out, n_blocks, compact, rk, ivs, 1, sms, s, tin, tiv);
+      if (dec) return launch_blocks_t<1, true, kIvRows, true>(in, out, n_blocks, compact, rk, ivs, 1, sms, s, tin, tiv, tsb);
+      return launch_blocks_t<1, false, kIvRows, true>(in, out, n_blocks, compact, rk, ivs, 1, sms, s, tin, tiv, tsb);
     }
-    if (dec) return launch_blocks_t<1, true, kIvRows, false>(in, out, n_blocks, compact, rk, ivs, 1, sms, s, 0, tiv);
-    return launch_blocks_t<1, false, kIvRows, false>(in, out, n_blocks, compact, rk, ivs, 1, sms, s, 0, tiv);
+    if (dec) return launch_blocks_t<1, true, kIvRows, false>(in, out, n_blocks, compact, rk, ivs, 1, sms, s, 0, tiv, tsb);
+    return launch_blocks_t<1, false, kIvRows, false>(in, out, n_blocks, compact, rk, ivs, 1, sms, s, 0, tiv, tsb);
   }
   if (tin && n_blocks <= 0x7FFFFFFFull) {
     if (ivmode == kIvFolded) {
-      if (dec) return launch_blocks_t<1, true, kIvFolded, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin);
-      return launch_blocks_t<1, false, kIvFolded, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin);
+      if (dec) return launch_blocks_t<1, true, kIvFolded, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin, 0, tsb);
+      return launch_blocks_t<1, false, kIvFolded, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin, 0, tsb);
     }
-    if (dec) return launch_blocks_t<1, true, kIvChain, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin);
-    return launch_blocks_t<1, false, kIvChain, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin);
+    if (dec) return launch_blocks_t<1, true, kIvChain, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin, 0, tsb);
+    return launch_blocks_t<1, false, kIvChain, true>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, tin, 0, tsb);
   }
   // Small batches: spread over every SM (one block per thread) rather than
   // giving few CTAs two blocks per thread; the 192 KiB table fill is per CTA.
   if ((uint64_t)sms * kBlockThreads * 8 > n_blocks) ilp = 1;
 #define GAES_CASE(I, D, M) \
-  if (ilp == I && dec == D && ivmode == M) return launch_blocks_t<I, D, M>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s);
+  if (ilp == I && dec == D && ivmode == M) return launch_blocks_t<I, D, M>(in, out, n_blocks, compact, rk, ivs, bpr, sms, s, 0, 0, tsb);
   GAES_CASE(1, false, kIvFolded) GAES_CASE(1, true, kIvFolded) GAES_CASE(1, false, kIvChain)
   GAES_CASE(1, true, kIvChain) GAES_CASE(2, false, kIvFolded) GAES_CASE(2, true, kIvFolded)
   GAES_CASE(2, false, kIvChain) GAES_CASE(2, true, kIvChain)
@@ -675,7 +678,7 @@ static void rows_geometry(uint64_t n_rows, int sms, int* grid, int* threads) {
 
 cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint64_t bpr, const uint32_t* compact,
                                 const RoundKeys& rk, const void* ivs, int sms, cudaStream_t s,
-                                cudaTextureObject_t tin) {
+                                cudaTextureObject_t tin, cudaTextureObject_t tsb) {
   if (n_rows == 0) return cudaSuccess;
   const bool pairs = bpr >= 2 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 31) == 0 &&
                      (bpr % 2 == 0);
@@ -690,7 +693,7 @@ cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint
   int grid = 0, threads = 0;
   rows_geometry(n_rows, sms, &grid, &threads);
   return launch_pdl(kern, grid, threads, kSmemBytes, s, (const uint4*)in, (uint4*)out, n_rows, bpr, compact, rk,
-                    (const uint4*)ivs, tin);
+                    (const uint4*)ivs, tin, tsb);
 }
 
 cudaError_t launch_generic(bool dec, const uint8_t* data, const uint8_t* ivs, uint64_t n, uint64_t m,
@@ -719,10 +722,10 @@ cudaError_t launch_bs_blocks(const void* in, void* out, uint64_t n_blocks, const
 }
 
 cudaError_t launch_round_probe(const uint32_t* compact, const RoundKeys& rk, uint32_t iters, uint32_t* sink,
-                               int sms, cudaStream_t s) {
+                               int sms, cudaStream_t s, cudaTextureObject_t tsb) {
   cudaError_t e = set_smem(k_round_probe);
   if (e != cudaSuccess) return e;
-  k_round_probe<<<sms, kBlockThreads, kSmemBytes, s>>>(compact, rk, iters, sink);
+  k_round_probe<<<sms, kBlockThreads, kSmemBytes, s>>>(compact, rk, iters, sink, tsb);
   return cudaGetLastError();
 }
 
@@ -744,7 +747,7 @@ cudaError_t launch_expand_keys(const uint8_t* keys, uint64_t k, const uint32_t* 
 
 cudaError_t launch_many_key(bool dec, const void* in, void* out, uint64_t n_blocks, uint64_t first, uint64_t bpk,
                             const uint32_t* compact, const void* rks, const void* ivs, int sms, cudaStream_t s,
-                            cudaTextureObject_t tin) {
+                            cudaTextureObject_t tin, cudaTextureObject_t tsb) {
   if (bpk == 0 || n_blocks == 0) return cudaSuccess;
   if (n_blocks > 0x7FFFFFFFull) tin = 0;
   auto kern = dec ? (tin ? k_many_key<true, true> : k_many_key<true, false>)
@@ -753,7 +756,7 @@ cudaError_t launch_many_key(bool dec, const void* in, void* out, uint64_t n_bloc
   if (e != cudaSuccess) return e;
   const int grid = grid_for(n_blocks, 1, sms, kManyKeyThreads);
   return launch_pdl(kern, grid, kManyKeyThreads, kSmemBytes, s, (const uint4*)in, (uint4*)out, n_blocks, first, bpk,
-                    compact, (const uint4*)rks, (const uint4*)ivs, tin);
+                    compact, (const uint4*)rks, (const uint4*)ivs, tin, tsb);
 }
 
 }  // namespace gaes

@@ -20,12 +20,15 @@ cudaError_t launch_gf_build(uint32_t* enc, uint32_t* dec, uint8_t* sbox, uint8_t
 cudaError_t launch_build_tables(const uint8_t* box, const uint8_t* lut, uint32_t* out, cudaStream_t s);
 // tin: optional linear texture over `in` (uint4 texels); tiv: optional
 // texture over `ivs` (per-row IVs with one block per row); 0 = plain LDG.
+// tsb: optional u8 texture of the S-box matching `compact` (round 10 then
+// reads it through the TEX pipe and the S table is not replicated in smem).
 cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* out, uint64_t n_blocks,
                           const uint32_t* compact, const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms,
-                          cudaStream_t s, cudaTextureObject_t tin = 0, cudaTextureObject_t tiv = 0);
+                          cudaStream_t s, cudaTextureObject_t tin = 0, cudaTextureObject_t tiv = 0,
+                          cudaTextureObject_t tsb = 0);
 cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint64_t bpr, const uint32_t* compact,
                                 const RoundKeys& rk, const void* ivs, int sms, cudaStream_t s,
-                                cudaTextureObject_t tin = 0);
+                                cudaTextureObject_t tin = 0, cudaTextureObject_t tsb = 0);
 cudaError_t launch_generic(bool dec, const uint8_t* data, const uint8_t* ivs, uint64_t n, uint64_t m,
                            const uint8_t* rk, const uint8_t* box, const uint8_t* lut, const uint8_t* perm,
                            uint8_t* out, int sms, cudaStream_t s);
@@ -33,13 +36,14 @@ struct BitsliceKeys;
 cudaError_t launch_bs_blocks(const void* in, void* out, uint64_t n_blocks, const BitsliceKeys& keys, int sms,
                              cudaStream_t s);
 cudaError_t launch_round_probe(const uint32_t* compact, const RoundKeys& rk, uint32_t iters, uint32_t* sink,
-                               int sms, cudaStream_t s);
+                               int sms, cudaStream_t s,
+                               cudaTextureObject_t tsb = 0);
 // Shared-memory lookup peak: 16 conflict-free LDS.32 per thread per iteration.
 cudaError_t launch_lds_peak(uint32_t iters, uint32_t* sink, int sms, cudaStream_t s);
 cudaError_t launch_expand_keys(const uint8_t* keys, uint64_t k, const uint32_t* compact_enc, uint8_t* rk_enc,
                                uint8_t* rk_dec, cudaStream_t s);
 cudaError_t launch_many_key(bool dec, const void* in, void* out, uint64_t n_blocks, uint64_t first, uint64_t bpk,
                             const uint32_t* compact, const void* rks, const void* ivs, int sms, cudaStream_t s,
-                            cudaTextureObject_t tin = 0);
+                            cudaTextureObject_t tin = 0, cudaTextureObject_t tsb = 0);
 
 }  // namespace gaes

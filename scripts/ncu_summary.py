@@ -29,6 +29,10 @@ KEYS = [
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput % of peak"),
     ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe (LDS/LDG/STG) % of peak"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "L1 data pipe, LSU wavefronts % of peak"),
+    ("l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed", "L1 data pipe, TEX wavefronts % of peak"),
+    ("sm__inst_executed_pipe_tex.avg.pct_of_peak_sustained_active", "TEX pipe (texture fetches) % of peak"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1/TEX throughput % of peak"),
     ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe (LOP3/PRMT/SHF) % of peak"),
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe (IMAD) % of peak"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
