@@ -1000,3 +1000,42 @@ def test_cuda_graph_capture_and_replay(oracle):
         assert np.array_equal(rows_ct.cpu().numpy(), oracle.encrypt(key, ivrows[: n // 4], pr, threads=4))
         for _ in range(70):  # churn the texture cache between replays
             device.encrypt_blocks(torch.empty((1024 + rep, 16), dtype=torch.uint8, device="cuda"), rk, iv)
+
+
+def test_shared_memory_sbox_path_without_textures():
+    """GAES_TEXS=0 / GAES_TEXIN=0 (the paths used when textures are
+    unavailable): round 10 reads the replicated S table in shared memory and
+    inputs come through LDG -- bit-exact against the oracle for every kernel."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, sys, torch
+sys.path.insert(0, ".")
+from oracle import oracle
+from paper_1506_08503_b200 import _lib, backend_cuda, device
+assert _lib.lib().gaes_uses_sbox_texture(0) == 0
+rng = np.random.default_rng(3)
+key, iv = rng.bytes(16), rng.bytes(16)
+rk = oracle.gen_keys(key)
+for n, m in [(70001, 16), (3001, 64)]:
+    p = rng.integers(0, 256, (n, m), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    want = oracle.encrypt(key, ivs, p, threads=4)
+    x = torch.from_numpy(p).cuda()
+    c = device.cbc_encrypt(x, rk, torch.from_numpy(ivs).cuda())
+    assert np.array_equal(c.cpu().numpy(), want)
+    assert torch.equal(device.cbc_decrypt(c, rk, torch.from_numpy(ivs).cuda()), x)
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (n, 1))
+    assert np.array_equal(backend_cuda.encrypt_shared_iv(p, iv, rk), oracle.encrypt(key, ivrows, p, threads=4))
+keys = rng.integers(0, 256, (4, 16), dtype=np.uint8)
+p = rng.integers(0, 256, (4 * 5000, 16), dtype=np.uint8)
+c = backend_cuda.many_key_encrypt(p, keys)
+assert np.array_equal(c[:5000], oracle.encrypt(keys[0].tobytes(), np.zeros((5000, 16), np.uint8), p[:5000]))
+assert np.array_equal(backend_cuda.many_key_decrypt(c, keys), p)
+print("ok")
+'''
+    env = dict(os.environ, GAES_TEXS="0", GAES_TEXIN="0")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
