@@ -753,6 +753,10 @@ def main():
                       + (" + 16 S-box byte fetches on the TEX pipe (round 10)" if tex_sbox else
                          " incl. round 10's 16 S-box lookups")),
         "lookups_per_block": {"shared_memory": lds_per_block, "texture": LOOKUPS_PER_BLOCK - lds_per_block},
+        "binding_note": ("the L1 data path is shared by the shared-memory T-table lookups (LSU side) and the "
+                         "S-box / input texture fetches (TEX side); ncu: LSU wavefronts 96 %, TEX wavefronts 84 %, "
+                         "l1tex__throughput 98 % (profiles/r1_final_ttable_ncu_summary.md)" if tex_sbox else
+                         "ncu: L1 LSU data pipe 96 % busy"),
         "peak_source": ("measured: gaes_probe_lds_peak (k_lds_peak, conflict-free LDS.32 stream on every lane, "
                         f"{sms} SMs x 1024 threads) in this run; MEASURED_PEAKS.json has no shared-memory figure"
                         if lds_measured else "nominal (probe unavailable): 32 LDS lanes/clk/SM x SMs x SM clock"),
