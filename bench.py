@@ -748,7 +748,10 @@ def main():
         "achieved": round(lds_achieved, 2), "peak": round(peak, 2), "unit": "Glookup/s",
         "frac": round(lds_achieved / peak, 4), "traffic": traffic,
         "traffic_unit": "GB per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, profiles/traffic.json)",
-        "algorithmic_gb_per_launch": round(n * HBM_BYTES_PER_BLOCK / 1e9, 4),
+        # a step may be several launches (device-API calls are cut into
+        # 2^28-block texture segments: config 5 = 4 launches per step)
+        "algorithmic_gb_per_launch": round(n * HBM_BYTES_PER_BLOCK / max(1, launches // max(1, args.steps)) / 1e9, 4),
+        "launches_per_step": max(1, launches // max(1, args.steps)),
         "per_block": (f"{lds_per_block} conflict-free 4-B LDS table lookups per 16-B block (rounds 1-9)"
                       + (" + 16 S-box byte fetches on the TEX pipe (round 10)" if tex_sbox else
                          " incl. round 10's 16 S-box lookups")),
