@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_PATH = os.path.join(PKG_DIR, "libgaes_b200.so")
 SOURCES = ["kernels.cu", "runtime.cpp", "device_ctx.cpp", "host_pipeline.cpp", "abi.cpp"]
 HEADERS = ["gf.cuh", "aes_ttable.cuh", "aes_bitslice.cuh", "kernels.h", "types.h", "host_pool.h", "round_keys.h",
-           "runtime.h", "device_ctx.h", "host_pipeline.h"]
+           "runtime.h", "device_ctx.h", "host_pipeline.h", "tma.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden",
                      "-Xptxas", "-O3", "-I", os.path.join(REPO, "include")]

@@ -25,6 +25,7 @@
 #include "aes_ttable.cuh"
 #include "gf.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace gaes {
 
@@ -297,6 +298,97 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
       }
     }
   }
+}
+
+// CBC encrypt along rows with the row tiles staged through shared memory by
+// TMA.  A warp owns 32 consecutive rows (lane = row, serial chain per row,
+// _kernel.pyx:29-54); per step it needs the next 2 blocks (32 bytes) of each
+// of its rows -- a 32-row x 32-byte box of the N x M grid.  One elected lane
+// moves that box with cp.async.bulk.tensor (double-buffered, completion on
+// an mbarrier) and the ciphertext box back the same way from a swizzled
+// staging tile, so the strided per-lane LDG.256 / STG.256 (one L1 wavefront
+// per lane) become conflict-free LDS.128 / STS.128 (4 wavefronts per 32
+// lanes) plus TMA traffic.  Needs the texture S-box: the T tables take
+// 128 KiB and the per-warp buffers (3 KiB) use the rest of shared memory.
+static constexpr int kRowsTmaTileBytes = 32 * 32;       // 32 rows x 32 bytes
+static constexpr int kRowsTmaWarpBytes = 3 * kRowsTmaTileBytes;  // 2 load buffers + 1 store buffer
+static constexpr int kTablesBytes = 2 * kRegionBytes;   // T0|T1, T2|T3
+
+__global__ void __launch_bounds__(kBlockThreads, 1)
+    k_cbc_enc_rows_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+                       uint64_t n_rows, uint64_t bpr, const uint32_t* __restrict__ compact,
+                       const __grid_constant__ RoundKeys rk, const uint4* __restrict__ ivs, cudaTextureObject_t tsb) {
+  extern __shared__ __align__(1024) char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  char* buf = smem + kTablesBytes + warp * kRowsTmaWarpBytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kTablesBytes + nwarps * kRowsTmaWarpBytes) + 2 * warp;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init_fence();
+  }
+  pdl_prologue(smem, compact, false);  // T tables only; ends with __syncthreads
+  const uint32_t lb = lane * 4;
+  const uint64_t pairs = bpr / 2;
+  const uint32_t o0 = swizzle32(lane * 32), o1 = swizzle32(lane * 32 + 16);
+  uint32_t phase0 = 0, phase1 = 0;
+  auto enc = [&](const uint4& p, uint4& c) {
+    uint32_t s0 = p.x ^ c.x ^ rk.w[0], s1 = p.y ^ c.y ^ rk.w[1];
+    uint32_t s2 = p.z ^ c.z ^ rk.w[2], s3 = p.w ^ c.w ^ rk.w[3];
+    encrypt_rounds(smem, lb, s0, s1, s2, s3, rk, tsb);
+    c = make_uint4(s0, s1, s2, s3);
+  };
+  const uint64_t groups = (n_rows + 31) / 32;
+  for (uint64_t g = (uint64_t)blockIdx.x * nwarps + warp; g < groups; g += (uint64_t)gridDim.x * nwarps) {
+    const int r0 = (int)(g * 32);
+    const uint64_t row = g * 32 + lane;
+    uint4 c = make_uint4(rk.iv[0], rk.iv[1], rk.iv[2], rk.iv[3]);
+    if (ivs && row < n_rows) c = __ldg(ivs + row);
+    if (lane == 0) {
+      mbar_expect_tx(&bar[0], kRowsTmaTileBytes);
+      tma_load_2d(buf, &tin, 0, r0, &bar[0]);
+      if (pairs > 1) {
+        mbar_expect_tx(&bar[1], kRowsTmaTileBytes);
+        tma_load_2d(buf + kRowsTmaTileBytes, &tin, 32, r0, &bar[1]);
+      }
+    }
+    for (uint64_t q = 0; q < pairs; q++) {
+      const int b = (int)(q & 1);
+      char* tile = buf + b * kRowsTmaTileBytes;
+      if (b == 0) {
+        mbar_wait(&bar[0], phase0);
+        phase0 ^= 1;
+      } else {
+        mbar_wait(&bar[1], phase1);
+        phase1 ^= 1;
+      }
+      const uint4 p0 = *reinterpret_cast<const uint4*>(tile + o0);
+      const uint4 p1 = *reinterpret_cast<const uint4*>(tile + o1);
+      __syncwarp();
+      if (lane == 0 && q + 2 < pairs) {  // refill this buffer two steps ahead
+        mbar_expect_tx(&bar[b], kRowsTmaTileBytes);
+        tma_load_2d(tile, &tin, (int)((q + 2) * 32), r0, &bar[b]);
+      }
+      uint4 c0 = c;
+      enc(p0, c0);
+      uint4 c1 = c0;
+      enc(p1, c1);
+      c = c1;
+      char* st = buf + 2 * kRowsTmaTileBytes;
+      if (lane == 0) bulk_wait_read<0>();  // the previous store has read the staging tile
+      __syncwarp();
+      *reinterpret_cast<uint4*>(st + o0) = c0;
+      *reinterpret_cast<uint4*>(st + o1) = c1;
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(&tout, (int)(q * 32), r0, st);
+        bulk_commit();
+      }
+    }
+  }
+  if (lane == 0) bulk_wait<0>();
 }
 
 // Byte-level CBC with arbitrary tables: a direct transcription of
@@ -676,10 +768,93 @@ static void rows_geometry(uint64_t n_rows, int sms, int* grid, int* threads) {
   *grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(sms, (per_wave + t - 1) / t));
 }
 
+static thread_local bool t_rows_tma = false;
+bool last_rows_launch_used_tma() { return t_rows_tma; }
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link
+// dependency on libcuda); nullptr if unavailable.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (EncodeTiledFn) nullptr;
+    }
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// n_rows x m-byte grid as a 2-D uint8 tensor, 32-row x 32-byte boxes,
+// 32-byte swizzle (conflict-free LDS.128/STS.128 of each lane's 32 bytes).
+static bool rows_tensor_map(CUtensorMap* map, const void* base, uint64_t n_rows, uint64_t m) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {m, n_rows};
+  const cuuint64_t strides[1] = {m};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// TMA row kernel: texture S-box, even blocks per row >= 8, 16-byte aligned
+// grids, coordinates inside int32; GAES_ROWS_TMA=0 disables it.
+static cudaError_t launch_cbc_enc_rows_tma(const void* in, void* out, uint64_t n_rows, uint64_t bpr,
+                                           const uint32_t* compact, const RoundKeys& rk, const void* ivs, int sms,
+                                           cudaStream_t s, cudaTextureObject_t tsb, bool* launched) {
+  *launched = false;
+  static const bool enabled = [] {
+    const char* e = std::getenv("GAES_ROWS_TMA");
+    return !(e && *e && std::atoi(e) == 0);
+  }();
+  const uint64_t m = bpr * 16;
+  if (!enabled || !tsb || bpr < 8 || (bpr & 1) || n_rows < 32 || n_rows > 0x7FFFFFF0ull || m > 0x7FFFFFF0ull ||
+      ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15))
+    return cudaSuccess;
+  // The double-buffered TMA pipeline needs many warps per SM to cover the
+  // load latency: with fewer than ~24 row groups per SM (long rows, few of
+  // them) the LDG/STG kernel is faster (2^16 rows of 256 blocks: 642 vs
+  // 669 GB/s; 2^18 rows of 64 blocks: 782 vs 719).
+  const uint64_t groups = (n_rows + 31) / 32;
+  if (groups < (uint64_t)sms * 24) return cudaSuccess;
+  CUtensorMap tmi, tmo;
+  if (!rows_tensor_map(&tmi, in, n_rows, m) || !rows_tensor_map(&tmo, out, n_rows, m)) return cudaSuccess;
+  // whole waves of 32-row groups (see rows_geometry): warps per CTA <= 32
+  const uint64_t cap = (uint64_t)sms * 32;
+  const uint64_t waves = (groups + cap - 1) / cap;
+  const uint64_t per_wave = (groups + waves - 1) / waves;
+  const int warps = (int)std::min<uint64_t>(32, std::max<uint64_t>(4, (per_wave + sms - 1) / sms));
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(sms, (per_wave + warps - 1) / warps));
+  const size_t smem = kTablesBytes + (size_t)warps * kRowsTmaWarpBytes + (size_t)warps * 16;
+  static std::once_flag once;
+  static cudaError_t attr = cudaSuccess;
+  std::call_once(once, [] {
+    attr = cudaFuncSetAttribute(k_cbc_enc_rows_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kTablesBytes + 32 * kRowsTmaWarpBytes + 32 * 16);
+  });
+  if (attr != cudaSuccess) return cudaSuccess;  // fall back to the LDG/STG kernel
+  *launched = true;
+  return launch_pdl(k_cbc_enc_rows_tma, grid, warps * 32, smem, s, tmi, tmo, n_rows, bpr, compact, rk,
+                    (const uint4*)ivs, tsb);
+}
+
 cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint64_t bpr, const uint32_t* compact,
                                 const RoundKeys& rk, const void* ivs, int sms, cudaStream_t s,
                                 cudaTextureObject_t tin, cudaTextureObject_t tsb) {
   if (n_rows == 0) return cudaSuccess;
+  {
+    bool launched = false;
+    cudaError_t e = launch_cbc_enc_rows_tma(in, out, n_rows, bpr, compact, rk, ivs, sms, s, tsb, &launched);
+    t_rows_tma = launched;
+    if (e != cudaSuccess || launched) return e;
+  }
   const bool pairs = bpr >= 2 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 31) == 0 &&
                      (bpr % 2 == 0);
   // texture loads measured +1.5% at 2-4 blocks per row and neutral to -2%

@@ -26,6 +26,9 @@ cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* o
                           const uint32_t* compact, const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms,
                           cudaStream_t s, cudaTextureObject_t tin = 0, cudaTextureObject_t tiv = 0,
                           cudaTextureObject_t tsb = 0);
+// Row CBC encrypt: the TMA-staged kernel when it applies (texture S-box,
+// >= 8 even blocks per row, enough rows), else the LDG/STG kernel.
+bool last_rows_launch_used_tma();  // on this thread
 cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint64_t bpr, const uint32_t* compact,
                                 const RoundKeys& rk, const void* ivs, int sms, cudaStream_t s,
                                 cudaTextureObject_t tin = 0, cudaTextureObject_t tsb = 0);

@@ -7,6 +7,7 @@ configs at full size through size-independent properties.
 """
 
 import hashlib
+import os
 import threading
 
 import numpy as np
@@ -1039,3 +1040,32 @@ print("ok")
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("blocks", [8, 10])
+def test_row_cbc_tma_path_matches_oracle(oracle, blocks):
+    """General-M CBC encrypt with enough rows for the TMA row kernel (>= 24
+    row groups of 32 per SM): ragged last group (TMA out-of-bounds rows),
+    shared and per-row IVs, device and host entry points."""
+    rng = np.random.default_rng(blocks)
+    key, iv = rng.bytes(16), rng.bytes(16)
+    rk = oracle.gen_keys(key)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    n = sms * 24 * 32 + 17
+    m = 16 * blocks
+    p = rng.integers(0, 256, (n, m), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    x = torch.from_numpy(p).cuda()
+    want = oracle.encrypt(key, ivs, p, threads=8)
+    c = device.cbc_encrypt(x, rk, torch.from_numpy(ivs).cuda())
+    if _lib.lib().gaes_uses_sbox_texture(0) == 1 and os.environ.get("GAES_ROWS_TMA", "1") != "0":
+        assert _lib.last_kernel() == "k_cbc_enc_rows_tma"
+    assert np.array_equal(c.cpu().numpy(), want)
+    assert torch.equal(device.cbc_decrypt(c, rk, torch.from_numpy(ivs).cuda()), x)
+    ivrows = np.tile(np.frombuffer(iv, np.uint8), (n, 1))
+    want_shared = oracle.encrypt(key, ivrows, p, threads=8)
+    assert np.array_equal(device.cbc_encrypt(x, rk, iv).cpu().numpy(), want_shared)
+    out = np.empty_like(p)
+    backend_cuda.cbc_encrypt(p, ivs, *oracle.encrypt_tables(key), out)   # host pipeline chunks
+    assert np.array_equal(out, want)
+    assert np.array_equal(backend_cuda.encrypt_shared_iv(p, iv, rk), want_shared)
