@@ -323,12 +323,15 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
   const int nwarps = blockDim.x >> 5;
   char* buf = smem + kTablesBytes + warp * kRowsTmaWarpBytes;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kTablesBytes + nwarps * kRowsTmaWarpBytes) + 2 * warp;
+  // The table fill stages the compact tables in the S region, which this
+  // kernel reuses for its tiles and barriers: initialise the barriers after it.
+  pdl_prologue(smem, compact, false);  // T tables only; ends with __syncthreads
   if (lane == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     mbar_init_fence();
   }
-  pdl_prologue(smem, compact, false);  // T tables only; ends with __syncthreads
+  __syncwarp();
   const uint32_t lb = lane * 4;
   const uint64_t pairs = bpr / 2;
   const uint32_t o0 = swizzle32(lane * 32), o1 = swizzle32(lane * 32 + 16);
@@ -822,8 +825,12 @@ static cudaError_t launch_cbc_enc_rows_tma(const void* in, void* out, uint64_t n
   // load latency: with fewer than ~24 row groups per SM (long rows, few of
   // them) the LDG/STG kernel is faster (2^16 rows of 256 blocks: 642 vs
   // 669 GB/s; 2^18 rows of 64 blocks: 782 vs 719).
+  static const uint64_t min_groups_per_sm = [] {
+    const char* e = std::getenv("GAES_ROWS_TMA_MIN_GROUPS");  // per SM; tests set 0
+    return (uint64_t)((e && *e) ? std::max(0, std::atoi(e)) : 24);
+  }();
   const uint64_t groups = (n_rows + 31) / 32;
-  if (groups < (uint64_t)sms * 24) return cudaSuccess;
+  if (groups < (uint64_t)sms * min_groups_per_sm) return cudaSuccess;
   CUtensorMap tmi, tmo;
   if (!rows_tensor_map(&tmi, in, n_rows, m) || !rows_tensor_map(&tmo, out, n_rows, m)) return cudaSuccess;
   // whole waves of 32-row groups (see rows_geometry): warps per CTA <= 32

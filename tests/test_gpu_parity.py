@@ -1069,3 +1069,33 @@ def test_row_cbc_tma_path_matches_oracle(oracle, blocks):
     backend_cuda.cbc_encrypt(p, ivs, *oracle.encrypt_tables(key), out)   # host pipeline chunks
     assert np.array_equal(out, want)
     assert np.array_equal(backend_cuda.encrypt_shared_iv(p, iv, rk), want_shared)
+
+
+def test_row_cbc_tma_kernel_at_any_row_count():
+    """The TMA row kernel itself (forced for every row count with
+    GAES_ROWS_TMA_MIN_GROUPS=0, normally only used from 24 row groups per
+    SM): 1..4 warps with rows, ragged groups, 8..64-block rows."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from oracle import oracle
+from paper_1506_08503_b200 import device, _lib
+rng = np.random.default_rng(9)
+key, iv = rng.bytes(16), rng.bytes(16)
+rk = oracle.gen_keys(key)
+for n, bpr in [(32, 8), (33, 64), (100, 16), (1500, 8), (4737, 10)]:
+    p = rng.integers(0, 256, (n, 16 * bpr), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    c = device.cbc_encrypt(torch.from_numpy(p).cuda(), rk, torch.from_numpy(ivs).cuda())
+    assert _lib.last_kernel() == "k_cbc_enc_rows_tma", _lib.last_kernel()
+    assert np.array_equal(c.cpu().numpy(), oracle.encrypt(key, ivs, p, threads=4)), (n, bpr)
+print("ok")
+'''
+    env = dict(os.environ, GAES_ROWS_TMA_MIN_GROUPS="0")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True, text=True, timeout=300)
+    if "k_cbc_enc_rows\n" in r.stderr or _lib.lib().gaes_uses_sbox_texture(0) != 1:
+        pytest.skip("texture S-box unavailable: the TMA row kernel does not apply")
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
