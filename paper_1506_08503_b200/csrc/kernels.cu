@@ -677,7 +677,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_
 // The 192 KiB opt-in is set once per (kernel, device); launching small
 // pipeline chunks must not pay a driver call each time.
 template <typename K>
-static cudaError_t set_smem(K kernel) {
+static cudaError_t set_smem(K kernel, int bytes = kSmemBytes) {
   static std::mutex mu;
   static std::set<std::pair<const void*, int>> done;
   int dev = 0;
@@ -686,7 +686,7 @@ static cudaError_t set_smem(K kernel) {
   const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
   std::lock_guard<std::mutex> lk(mu);
   if (done.count(key)) return cudaSuccess;
-  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) done.insert(key);
   return e;
 }
@@ -840,13 +840,11 @@ static cudaError_t launch_cbc_enc_rows_tma(const void* in, void* out, uint64_t n
   const int warps = (int)std::min<uint64_t>(32, std::max<uint64_t>(4, (per_wave + sms - 1) / sms));
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(sms, (per_wave + warps - 1) / warps));
   const size_t smem = kTablesBytes + (size_t)warps * kRowsTmaWarpBytes + (size_t)warps * 16;
-  static std::once_flag once;
-  static cudaError_t attr = cudaSuccess;
-  std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(k_cbc_enc_rows_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kTablesBytes + 32 * kRowsTmaWarpBytes + 32 * 16);
-  });
-  if (attr != cudaSuccess) return cudaSuccess;  // fall back to the LDG/STG kernel
+  // per (kernel, device), like every other 192 KiB+ kernel
+  if (set_smem(k_cbc_enc_rows_tma, kTablesBytes + 32 * kRowsTmaWarpBytes + 32 * 16) != cudaSuccess) {
+    cudaGetLastError();
+    return cudaSuccess;  // fall back to the LDG/STG kernel
+  }
   *launched = true;
   return launch_pdl(k_cbc_enc_rows_tma, grid, warps * 32, smem, s, tmi, tmo, n_rows, bpr, compact, rk,
                     (const uint4*)ivs, tsb);
