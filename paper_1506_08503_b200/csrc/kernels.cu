@@ -1,15 +1,20 @@
 // kernels.cu -- sm_100a kernels of the AES-128 hot path.
 //
-//   k_gf_build        GF(2^8) layer: S, S^-1, Te, Td from field arithmetic
-//   k_build_tables    T tables from the tables the reference hands over
-//   k_blocks          M = 16 blocks (and block-parallel CBC decrypt), T-table
-//   k_cbc_enc_rows    CBC encrypt along rows (serial chain, M > 16)
-//   k_generic_cbc     byte-level round for arbitrary shift permutations /
-//                     non-linear mix tables (correctness path, still GPU)
-//   k_expand_keys     batched key schedule (key_schedule.py:50-70)
-//   k_many_key        many-key batch (config 5)
-//   k_bs_blocks       bitsliced LOP3 encrypt (variant 2, for comparison)
-//   k_round_probe     roofline probe: the round function without HBM traffic
+//   k_gf_build          GF(2^8) layer: S, S^-1, Te, Td from field arithmetic
+//   k_build_tables      T tables from the tables the reference hands over
+//   k_blocks            M = 16 blocks, per-message IVs and block-parallel CBC
+//                       decrypt: T tables in shared memory (rounds 1-9), S-box
+//                       through a texture (round 10), inputs through textures
+//   k_cbc_enc_rows_tma  CBC encrypt along rows (serial chain, M > 16) with the
+//                       row tiles staged through shared memory by TMA
+//   k_cbc_enc_rows      the same with per-lane 256-bit LDG/STG (few long rows)
+//   k_generic_cbc       byte-level round for arbitrary shift permutations /
+//                       non-linear mix tables (correctness path, still GPU)
+//   k_expand_keys       batched key schedule (key_schedule.py:50-70)
+//   k_many_key          many-key batch (config 5)
+//   k_bs_blocks         bitsliced LOP3 encrypt (variant 2, for comparison)
+//   k_round_probe       roofline probe: the round function without HBM traffic
+//   k_lds_peak          roofline denominator: conflict-free LDS.32 stream
 //
 // Reference semantics: pkg/src/gaes/_kernel.pyx:12-101.
 #include <cuda_runtime.h>
