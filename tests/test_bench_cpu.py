@@ -36,3 +36,10 @@ def test_multi_gpu_request_without_gpus_fails_loudly():
     r = subprocess.run([sys.executable, "bench.py", "--gpus", "2"], cwd=REPO, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 2 and "needs 2 visible GPUs" in r.stderr
+
+
+def test_metric_is_baselines_verbatim():
+    import json
+    import bench
+    with open(os.path.join(REPO, "BASELINE.json")) as f:
+        assert bench.METRIC == json.load(f)["metric"]
