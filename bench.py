@@ -418,6 +418,179 @@ def run_reference_impl(args):
 
 # ----------------------------------------------------------------------------- ours
 
+def host_api_legs(args, inp, p, n, iv, rk, ch, w, total_blocks, world, rank, dev, launched):
+    """`e2e` (the public host-buffer API with pinned buffers, H2D + kernel +
+    D2H inside every timed step) and `e2e_dropin` (the reference's 7-argument
+    backend call with pageable numpy buffers).  Returns (e2e, dropin, ok)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1506_08503_b200 import backend_cuda
+    from paper_1506_08503_b200.shard import max_over_ranks
+
+    ok = True
+    # ---- e2e through the public host-buffer API (pinned host memory)
+    e2e = None
+    if not args.no_e2e and args.config == 5:
+        # config 5 end to end: keys + data from pinned host memory through the
+        # host many-key entry point (key schedule on the GPU inside the step)
+        h_in = torch.empty((n, 16), dtype=torch.uint8).pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        h_in.copy_(p)
+        hi, ho = h_in.numpy(), h_out.numpy()
+        backend_cuda.many_key_encrypt(hi, inp["keys"], inp["ivs"], out=ho)
+        if launched:
+            dist.barrier()
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            backend_cuda.many_key_encrypt(hi, inp["keys"], inp["ivs"], out=ho)
+            ts.append(time.perf_counter() - t0)
+        e2e_s = max_over_ranks(sum(ts) / len(ts), dev)
+        ok &= bool(np.array_equal(ho[:4096], ch[:4096]))
+        e2e = {"value": total_blocks * BYTES_PER_BLOCK / e2e_s / 1e9, "unit": "GB/s",
+               "step_ms": [round(t * 1e3, 3) for t in ts],
+               "h2d_bytes_per_step": int(n * 16 + inp["keys"].size + inp["ivs"].size),
+               "d2h_bytes_per_step": int(n * 16),
+               "api": "backend_cuda.many_key_encrypt -> gaes_many_key_encrypt (pinned host buffers, "
+                      "GPU key schedule per step)"}
+        del h_in, h_out
+    if not args.no_e2e and args.config != 5:
+        n_e2e = n
+        h_in = torch.empty((n_e2e, 16), dtype=torch.uint8).pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        h_in.copy_(p[:n_e2e])
+        hi, ho = h_in.numpy(), h_out.numpy()
+        for _ in range(2):
+            backend_cuda.encrypt_shared_iv(hi, iv, rk, out=ho)
+        if launched:
+            dist.barrier()
+        ts = []
+        for _ in range(max(3, min(args.steps, 10))):
+            t0 = time.perf_counter()
+            backend_cuda.encrypt_shared_iv(hi, iv, rk, out=ho)
+            ts.append(time.perf_counter() - t0)
+        e2e_s = max_over_ranks(sum(ts) / len(ts), dev)
+        e2e_blocks = n_e2e * world if w["scaling"] == "weak" else total_blocks
+        ok &= bool(np.array_equal(ho[:4096], ch[:4096]))
+        e2e = {"value": e2e_blocks * BYTES_PER_BLOCK / e2e_s / 1e9, "unit": "GB/s",
+               "step_ms": [round(t * 1e3, 3) for t in ts],
+               "h2d_bytes_per_step": int(n_e2e * 16), "d2h_bytes_per_step": int(n_e2e * 16),
+               "api": "backend_cuda.encrypt_shared_iv -> gaes_encrypt_shared_iv (pinned host buffers)"}
+
+    # ---- drop-in contract: the 7-argument backend call the reference's
+    # encrypt_batch makes (aes_cbc.py:352-355): pageable numpy buffers,
+    # IVSet.rows-tiled IVs, tables as _encrypt_tables builds them.
+    dropin = None
+    if not args.no_e2e and args.config != 5 and rank == 0:
+        n_d = min(n, 1 << 22)
+        hp = p[:n_d].cpu().numpy()
+        ivrows = np.tile(np.frombuffer(iv, np.uint8), (n_d, 1))
+        tables = (rk,) + backend_cuda.standard_tables(False)  # what _encrypt_tables(key) hands over
+        hout = np.empty_like(hp)
+        backend_cuda.cbc_encrypt(hp, ivrows, *tables, hout)
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            backend_cuda.cbc_encrypt(hp, ivrows, *tables, hout)
+            ts.append(time.perf_counter() - t0)
+        ok &= bool(np.array_equal(hout[:4096], ch[:4096]))
+        dropin = {"value": round(n_d * BYTES_PER_BLOCK / statistics.median(ts) / 1e9, 2), "unit": "GB/s",
+                  "blocks": n_d, "h2d_bytes_per_step": int(n_d * 16), "d2h_bytes_per_step": int(n_d * 16),
+                  "api": "backend_cuda.cbc_encrypt(data, ivs, round_keys, sbox, mix_lut, shift_src, out), "
+                         "pageable numpy buffers (reference backend contract)"}
+    return e2e, dropin, ok
+
+
+def roofline_for(args, n, ms_local, clocks, dev, local, step, launches):
+    """Roofline of the dominant kernel: shared-memory lookups/s against the
+    peak measured in this run (gaes_probe_lds_peak), with the nominal figure,
+    the formulation probe, the DRAM traffic from profiles/traffic.json and
+    the HBM fraction nested."""
+    import ctypes
+
+    import torch
+
+    from paper_1506_08503_b200 import _lib
+    sm_mhz = clocks.get("sm_mhz") or 1965.0
+    peaks = {}
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    per_gpu_blocks_s = n / (ms_local / 1e3)
+    # which lookups the L1/shared data pipe serves: round 10's 16 S-box
+    # fetches go through the texture path when the library says so
+    tex_sbox = _lib.lib().gaes_uses_sbox_texture(local) == 1
+    lds_per_block = T_LOOKUPS_PER_BLOCK if tex_sbox else LOOKUPS_PER_BLOCK
+    lds_achieved = per_gpu_blocks_s * lds_per_block / 1e9
+    lds_peak = sms * 32 * sm_mhz * 1e6 / 1e9
+    hbm_achieved = per_gpu_blocks_s * HBM_BYTES_PER_BLOCK / 1e9
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(f"cfg{args.config}")
+        except (OSError, ValueError):
+            traffic = None
+    probe = lds_measured = None
+    # the host-side legs above leave the GPU idle; bring the clocks back to
+    # the timed region's before measuring the roofline denominators
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 0.3:
+        step()
+        torch.cuda.synchronize()
+    try:
+        rate, pms = ctypes.c_double(), ctypes.c_double()
+        _lib.check(_lib.lib().gaes_probe_round_rate(local, 256, ctypes.addressof(rate), ctypes.addressof(pms)))
+        probe = rate.value / 1e9
+        # the roofline denominator, measured on this GPU in this run: a
+        # conflict-free LDS.32 stream on every lane of every SM
+        _lib.check(_lib.lib().gaes_probe_lds_peak(local, 4096, ctypes.addressof(rate), ctypes.addressof(pms)))
+        lds_measured = rate.value / 1e9
+    except Exception:  # pragma: no cover - informational only
+        pass
+    peak = lds_measured or lds_peak
+    roofline = {
+        "bound": "smem", "kernel": "k_blocks_enc_folded" if args.config != 5 else "k_many_key_enc",
+        "achieved": round(lds_achieved, 2), "peak": round(peak, 2), "unit": "Glookup/s",
+        "frac": round(lds_achieved / peak, 4), "traffic": traffic,
+        "traffic_unit": "GB per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, profiles/traffic.json)",
+        # a step may be several launches (device-API calls are cut into
+        # 2^28-block texture segments: config 5 = 4 launches per step)
+        "algorithmic_gb_per_launch": round(n * HBM_BYTES_PER_BLOCK / max(1, launches // max(1, args.steps)) / 1e9, 4),
+        "launches_per_step": max(1, launches // max(1, args.steps)),
+        "per_block": (f"{lds_per_block} conflict-free 4-B LDS table lookups per 16-B block (rounds 1-9)"
+                      + (" + 16 S-box byte fetches on the TEX pipe (round 10)" if tex_sbox else
+                         " incl. round 10's 16 S-box lookups")),
+        "lookups_per_block": {"shared_memory": lds_per_block, "texture": LOOKUPS_PER_BLOCK - lds_per_block},
+        "binding_note": ("the L1 data path is shared by the shared-memory T-table lookups (LSU side) and the "
+                         "S-box / input texture fetches (TEX side); ncu: LSU wavefronts 96 %, TEX wavefronts 84 %, "
+                         "l1tex__throughput 98 % (profiles/r1_final_ttable_ncu_summary.md)" if tex_sbox else
+                         "ncu: L1 LSU data pipe 96 % busy"),
+        "peak_source": ("measured: gaes_probe_lds_peak (k_lds_peak, conflict-free LDS.32 stream on every lane, "
+                        f"{sms} SMs x 1024 threads) in this run; MEASURED_PEAKS.json has no shared-memory figure"
+                        if lds_measured else "nominal (probe unavailable): 32 LDS lanes/clk/SM x SMs x SM clock"),
+        "nominal_peak": round(lds_peak, 2),
+        "nominal_frac": round(lds_achieved / lds_peak, 4),
+        "nominal_note": f"{sms} SMs x 32 lanes/clk x {sm_mhz:.0f} MHz (median SM clock sampled during the timed region)",
+        "probe_round_rate": round(probe * lds_per_block / LOOKUPS_PER_BLOCK, 2) if probe else None,
+        "probe_frac": round(lds_achieved / (probe * lds_per_block / LOOKUPS_PER_BLOCK), 4) if probe else None,
+        "probe_note": "k_round_probe: same round function (same S-box path) on register-resident states, no HBM "
+                      "(formulation ceiling, in shared-memory lookups/s)",
+        "hbm": {"achieved": round(hbm_achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(hbm_achieved / hbm_peak, 4),
+                "per_block": f"{HBM_BYTES_PER_BLOCK} B (16 read + 16 written)",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
+    }
+
+    return roofline
+
+
 def _relaunch_under_torchrun(n: int) -> int:
     """`python bench.py --gpus N` (N > 1) outside torchrun: re-run this same
     command as N ranks, one per GPU, over 127.0.0.1 (what the driver does)."""
@@ -629,154 +802,12 @@ def main():
         dec_ms = ev0.elapsed_time(ev1) / dreps
     dec_gbs = n * BYTES_PER_BLOCK / (dec_ms / 1e3) / 1e9
 
-    # ---- e2e through the public host-buffer API (pinned host memory)
-    e2e = None
-    if not args.no_e2e and args.config == 5:
-        # config 5 end to end: keys + data from pinned host memory through the
-        # host many-key entry point (key schedule on the GPU inside the step)
-        h_in = torch.empty((n, 16), dtype=torch.uint8).pin_memory()
-        h_out = torch.empty_like(h_in).pin_memory()
-        h_in.copy_(p)
-        hi, ho = h_in.numpy(), h_out.numpy()
-        backend_cuda.many_key_encrypt(hi, inp["keys"], inp["ivs"], out=ho)
-        if launched:
-            dist.barrier()
-        ts = []
-        for _ in range(3):
-            t0 = time.perf_counter()
-            backend_cuda.many_key_encrypt(hi, inp["keys"], inp["ivs"], out=ho)
-            ts.append(time.perf_counter() - t0)
-        e2e_s = max_over_ranks(sum(ts) / len(ts), dev)
-        verified &= bool(np.array_equal(ho[:4096], ch[:4096]))
-        e2e = {"value": total_blocks * BYTES_PER_BLOCK / e2e_s / 1e9, "unit": "GB/s",
-               "step_ms": [round(t * 1e3, 3) for t in ts],
-               "h2d_bytes_per_step": int(n * 16 + inp["keys"].size + inp["ivs"].size),
-               "d2h_bytes_per_step": int(n * 16),
-               "api": "backend_cuda.many_key_encrypt -> gaes_many_key_encrypt (pinned host buffers, "
-                      "GPU key schedule per step)"}
-        del h_in, h_out
-    if not args.no_e2e and args.config != 5:
-        n_e2e = n
-        h_in = torch.empty((n_e2e, 16), dtype=torch.uint8).pin_memory()
-        h_out = torch.empty_like(h_in).pin_memory()
-        h_in.copy_(p[:n_e2e])
-        hi, ho = h_in.numpy(), h_out.numpy()
-        for _ in range(2):
-            backend_cuda.encrypt_shared_iv(hi, iv, rk, out=ho)
-        if launched:
-            dist.barrier()
-        ts = []
-        for _ in range(max(3, min(args.steps, 10))):
-            t0 = time.perf_counter()
-            backend_cuda.encrypt_shared_iv(hi, iv, rk, out=ho)
-            ts.append(time.perf_counter() - t0)
-        e2e_s = max_over_ranks(sum(ts) / len(ts), dev)
-        e2e_blocks = n_e2e * world if w["scaling"] == "weak" else total_blocks
-        verified &= bool(np.array_equal(ho[:4096], ch[:4096]))
-        e2e = {"value": e2e_blocks * BYTES_PER_BLOCK / e2e_s / 1e9, "unit": "GB/s",
-               "step_ms": [round(t * 1e3, 3) for t in ts],
-               "h2d_bytes_per_step": int(n_e2e * 16), "d2h_bytes_per_step": int(n_e2e * 16),
-               "api": "backend_cuda.encrypt_shared_iv -> gaes_encrypt_shared_iv (pinned host buffers)"}
+    # ---- e2e legs through the public host-buffer API
+    e2e, dropin, ok = host_api_legs(args, inp, p, n, iv, rk, ch, w, total_blocks, world, rank, dev, launched)
+    verified &= ok
 
-    # ---- drop-in contract: the 7-argument backend call the reference's
-    # encrypt_batch makes (aes_cbc.py:352-355): pageable numpy buffers,
-    # IVSet.rows-tiled IVs, tables as _encrypt_tables builds them.
-    dropin = None
-    if not args.no_e2e and args.config != 5 and rank == 0:
-        n_d = min(n, 1 << 22)
-        hp = p[:n_d].cpu().numpy()
-        ivrows = np.tile(np.frombuffer(iv, np.uint8), (n_d, 1))
-        tables = (rk,) + backend_cuda.standard_tables(False)  # what _encrypt_tables(key) hands over
-        hout = np.empty_like(hp)
-        backend_cuda.cbc_encrypt(hp, ivrows, *tables, hout)
-        ts = []
-        for _ in range(5):
-            t0 = time.perf_counter()
-            backend_cuda.cbc_encrypt(hp, ivrows, *tables, hout)
-            ts.append(time.perf_counter() - t0)
-        verified &= bool(np.array_equal(hout[:4096], ch[:4096]))
-        dropin = {"value": round(n_d * BYTES_PER_BLOCK / statistics.median(ts) / 1e9, 2), "unit": "GB/s",
-                  "blocks": n_d, "h2d_bytes_per_step": int(n_d * 16), "d2h_bytes_per_step": int(n_d * 16),
-                  "api": "backend_cuda.cbc_encrypt(data, ivs, round_keys, sbox, mix_lut, shift_src, out), "
-                         "pageable numpy buffers (reference backend contract)"}
-
-    # ---- roofline of the dominant kernel (k_blocks encrypt): one launch per step
-    sm_mhz = clocks.get("sm_mhz") or 1965.0
-    peaks = {}
-    try:
-        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except OSError:
-        pass
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    per_gpu_blocks_s = n / (ms_local / 1e3)
-    # which lookups the L1/shared data pipe serves: round 10's 16 S-box
-    # fetches go through the texture path when the library says so
-    tex_sbox = _lib.lib().gaes_uses_sbox_texture(local) == 1
-    lds_per_block = T_LOOKUPS_PER_BLOCK if tex_sbox else LOOKUPS_PER_BLOCK
-    lds_achieved = per_gpu_blocks_s * lds_per_block / 1e9
-    lds_peak = sms * 32 * sm_mhz * 1e6 / 1e9
-    hbm_achieved = per_gpu_blocks_s * HBM_BYTES_PER_BLOCK / 1e9
-    traffic = None
-    tpath = os.path.join(REPO, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            with open(tpath) as f:
-                traffic = json.load(f).get(f"cfg{args.config}")
-        except (OSError, ValueError):
-            traffic = None
-    probe = lds_measured = None
-    # the host-side legs above leave the GPU idle; bring the clocks back to
-    # the timed region's before measuring the roofline denominators
-    t_soak = time.perf_counter()
-    while time.perf_counter() - t_soak < 0.3:
-        step()
-        torch.cuda.synchronize()
-    try:
-        import ctypes
-        rate, pms = ctypes.c_double(), ctypes.c_double()
-        _lib.check(_lib.lib().gaes_probe_round_rate(local, 256, ctypes.addressof(rate), ctypes.addressof(pms)))
-        probe = rate.value / 1e9
-        # the roofline denominator, measured on this GPU in this run: a
-        # conflict-free LDS.32 stream on every lane of every SM
-        _lib.check(_lib.lib().gaes_probe_lds_peak(local, 4096, ctypes.addressof(rate), ctypes.addressof(pms)))
-        lds_measured = rate.value / 1e9
-    except Exception:  # pragma: no cover - informational only
-        pass
-    peak = lds_measured or lds_peak
-    roofline = {
-        "bound": "smem", "kernel": "k_blocks_enc_folded" if args.config != 5 else "k_many_key_enc",
-        "achieved": round(lds_achieved, 2), "peak": round(peak, 2), "unit": "Glookup/s",
-        "frac": round(lds_achieved / peak, 4), "traffic": traffic,
-        "traffic_unit": "GB per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, profiles/traffic.json)",
-        # a step may be several launches (device-API calls are cut into
-        # 2^28-block texture segments: config 5 = 4 launches per step)
-        "algorithmic_gb_per_launch": round(n * HBM_BYTES_PER_BLOCK / max(1, launches // max(1, args.steps)) / 1e9, 4),
-        "launches_per_step": max(1, launches // max(1, args.steps)),
-        "per_block": (f"{lds_per_block} conflict-free 4-B LDS table lookups per 16-B block (rounds 1-9)"
-                      + (" + 16 S-box byte fetches on the TEX pipe (round 10)" if tex_sbox else
-                         " incl. round 10's 16 S-box lookups")),
-        "lookups_per_block": {"shared_memory": lds_per_block, "texture": LOOKUPS_PER_BLOCK - lds_per_block},
-        "binding_note": ("the L1 data path is shared by the shared-memory T-table lookups (LSU side) and the "
-                         "S-box / input texture fetches (TEX side); ncu: LSU wavefronts 96 %, TEX wavefronts 84 %, "
-                         "l1tex__throughput 98 % (profiles/r1_final_ttable_ncu_summary.md)" if tex_sbox else
-                         "ncu: L1 LSU data pipe 96 % busy"),
-        "peak_source": ("measured: gaes_probe_lds_peak (k_lds_peak, conflict-free LDS.32 stream on every lane, "
-                        f"{sms} SMs x 1024 threads) in this run; MEASURED_PEAKS.json has no shared-memory figure"
-                        if lds_measured else "nominal (probe unavailable): 32 LDS lanes/clk/SM x SMs x SM clock"),
-        "nominal_peak": round(lds_peak, 2),
-        "nominal_frac": round(lds_achieved / lds_peak, 4),
-        "nominal_note": f"{sms} SMs x 32 lanes/clk x {sm_mhz:.0f} MHz (median SM clock sampled during the timed region)",
-        "probe_round_rate": round(probe * lds_per_block / LOOKUPS_PER_BLOCK, 2) if probe else None,
-        "probe_frac": round(lds_achieved / (probe * lds_per_block / LOOKUPS_PER_BLOCK), 4) if probe else None,
-        "probe_note": "k_round_probe: same round function (same S-box path) on register-resident states, no HBM "
-                      "(formulation ceiling, in shared-memory lookups/s)",
-        "hbm": {"achieved": round(hbm_achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(hbm_achieved / hbm_peak, 4),
-                "per_block": f"{HBM_BYTES_PER_BLOCK} B (16 read + 16 written)",
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
-    }
+    # ---- roofline of the dominant kernel (k_blocks encrypt)
+    roofline = roofline_for(args, n, ms_local, clocks, dev, local, step, launches)
 
     cpu = None
     openssl = None
