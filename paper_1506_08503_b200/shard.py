@@ -89,28 +89,57 @@ def sum_over_ranks(value: int, device=None) -> int:
     return int(t.item())
 
 
+def parse_cpulist(text: str) -> list:
+    """CPU ids from a sysfs cpulist ("0-3,8,10-11")."""
+    cpus = []
+    for part in text.strip().split(","):
+        if "-" in part:
+            lo, hi = part.split("-")
+            cpus.extend(range(int(lo), int(hi) + 1))
+        elif part:
+            cpus.append(int(part))
+    return cpus
+
+
+def host_threads_per_rank(n_cpus: int, ranks_sharing: int) -> int:
+    """Copy threads for one rank when `ranks_sharing` ranks run on the same
+    `n_cpus` CPUs: an even share, so N ranks' spinning host pools
+    (csrc/host_pool.h) never oversubscribe a NUMA node."""
+    return max(1, n_cpus // max(1, ranks_sharing))
+
+
+def _gpu_cpulist(device_index: int) -> str:
+    import torch
+    props = torch.cuda.get_device_properties(device_index)
+    bdf = f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+    with open(f"/sys/bus/pci/devices/{bdf}/local_cpulist") as f:
+        return f.read().strip()
+
+
 def bind_to_gpu_numa_node(device_index: int) -> list | None:
     """Pin this process to the CPUs local to the GPU's PCIe root (one process
     per GPU): pinned staging buffers and host copies then stay on the GPU's
-    NUMA node.  Best effort; returns the CPU list used or None."""
+    NUMA node.  The host copy pool is sized to this rank's share of those
+    CPUs (GAES_HOST_THREADS, unless the caller set it): the local ranks whose
+    GPUs hang off the same node split its CPUs evenly.  Best effort; returns
+    the CPU list used or None."""
+    allowed = os.sched_getaffinity(0)
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", 1))
     try:
-        import torch
-        props = torch.cuda.get_device_properties(device_index)
-        bdf = f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
-        with open(f"/sys/bus/pci/devices/{bdf}/local_cpulist") as f:
-            text = f.read().strip()
-        cpus = []
-        for part in text.split(","):
-            if "-" in part:
-                lo, hi = part.split("-")
-                cpus.extend(range(int(lo), int(hi) + 1))
-            elif part:
-                cpus.append(int(part))
-        allowed = os.sched_getaffinity(0)
-        cpus = [c for c in cpus if c in allowed]
-        if not cpus or len(cpus) == len(allowed):
-            return None
+        mine = _gpu_cpulist(device_index)
+        sharing = 0
+        for g in range(local_world):
+            try:
+                sharing += _gpu_cpulist(g) == mine
+            except (OSError, RuntimeError, AssertionError):
+                pass
+        cpus = [c for c in parse_cpulist(mine) if c in allowed]
+    except (OSError, ValueError, AttributeError, RuntimeError, AssertionError):
+        cpus, sharing = [], local_world
+    bound = bool(cpus) and len(cpus) != len(allowed)
+    if bound:
         os.sched_setaffinity(0, cpus)
-        return cpus
-    except (OSError, ValueError, AttributeError, RuntimeError):
-        return None
+    if local_world > 1 and not os.environ.get("GAES_HOST_THREADS"):
+        pool = cpus if bound else sorted(allowed)
+        os.environ["GAES_HOST_THREADS"] = str(host_threads_per_rank(len(pool), max(1, sharing)))
+    return cpus if bound else None

@@ -105,3 +105,26 @@ def test_numa_binding_is_best_effort():
     before = os.sched_getaffinity(0)
     assert bind_to_gpu_numa_node(0) is None
     assert os.sched_getaffinity(0) == before
+
+
+def test_cpulist_and_per_rank_host_threads():
+    from paper_1506_08503_b200.shard import host_threads_per_rank, parse_cpulist
+    assert parse_cpulist("0-3,8,10-11\n") == [0, 1, 2, 3, 8, 10, 11]
+    assert parse_cpulist("") == []
+    assert host_threads_per_rank(56, 4) == 14
+    assert host_threads_per_rank(3, 8) == 1
+    assert host_threads_per_rank(16, 0) == 16
+
+
+def test_local_ranks_split_the_host_pool(monkeypatch):
+    # 4 local ranks and no GPU sysfs entry: every rank gets a quarter of the
+    # CPUs it may run on, and a caller's explicit GAES_HOST_THREADS wins
+    from paper_1506_08503_b200.shard import bind_to_gpu_numa_node
+    n = len(os.sched_getaffinity(0))
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "4")
+    monkeypatch.delenv("GAES_HOST_THREADS", raising=False)
+    assert bind_to_gpu_numa_node(0) is None
+    assert os.environ["GAES_HOST_THREADS"] == str(max(1, n // 4))
+    monkeypatch.setenv("GAES_HOST_THREADS", "7")
+    bind_to_gpu_numa_node(0)
+    assert os.environ["GAES_HOST_THREADS"] == "7"
