@@ -8,6 +8,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -184,6 +187,50 @@ std::unique_lock<std::mutex> lock_lane(DevCtx* c, Lane** out) {
   return std::unique_lock<std::mutex>(c->lanes[k].mu);
 }
 
+// Optional pipeline timeline (GAES_TRACE=<csv path>, measurement only): per
+// staged chunk, device events before the H2D and after the H2D, the kernel
+// and the D2H, appended to the file as ms relative to the first chunk.
+struct Trace {
+  const char* path = nullptr;
+  std::vector<cudaEvent_t> ev;  // 4 per chunk
+  std::vector<size_t> bytes;
+  std::vector<double> host;  // 3 per chunk: slot wait begins, slot free, chunk issued (ms)
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit Trace(size_t nchunks) {
+    path = std::getenv("GAES_TRACE");
+    if (!path || !*path) {
+      path = nullptr;
+      return;
+    }
+    ev.resize(4 * nchunks);
+    for (auto& e : ev) cudaEventCreate(&e);
+    bytes.resize(nchunks);
+    host.resize(3 * nchunks);
+  }
+  void host_mark(size_t ci, int k) {
+    if (path)
+      host[3 * ci + k] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  void mark(size_t ci, int k, cudaStream_t s) {
+    if (path) cudaEventRecord(ev[4 * ci + k], s);
+  }
+  ~Trace() {
+    if (!path) return;
+    cudaDeviceSynchronize();
+    if (FILE* f = std::fopen(path, "a")) {
+      std::fprintf(f, "chunk,bytes,h2d_start,h2d_end,kernel_end,d2h_end,host_wait,host_free,host_issued\n");
+      for (size_t ci = 0; ci < bytes.size(); ci++) {
+        float t[4] = {0, 0, 0, 0};
+        for (int k = 0; k < 4; k++) cudaEventElapsedTime(&t[k], ev[0], ev[4 * ci + k]);
+        std::fprintf(f, "%zu,%zu,%.4f,%.4f,%.4f,%.4f,%.4f,%.4f,%.4f\n", ci, bytes[ci], t[0], t[1], t[2], t[3],
+                     host[3 * ci] - host[0], host[3 * ci + 1] - host[0], host[3 * ci + 2] - host[0]);
+      }
+      std::fclose(f);
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
 // Runs rows [0, j.n) of `j` on device context c (one shard).
 int run_job(DevCtx* c, const Job& j) {
   if (j.n == 0) return GAES_OK;
@@ -312,12 +359,15 @@ int run_job(DevCtx* c, const Job& j) {
     if (rc) return rc;
   }
   int rc_final = GAES_OK;
+  Trace trace(nchunks);
   for (size_t ci = 0; ci < nchunks; ci++) {
     Slot& s = lane->slots[ci % kSlots];
+    trace.host_mark(ci, 0);
     if (ci >= (size_t)kSlots) {
       int rc = finish_slot(s);
       if (rc) return rc;
     }
+    trace.host_mark(ci, 1);
     const size_t r0 = chunks[ci].first;
     const size_t rows = chunks[ci].second;
     const size_t off = r0 * j.m, bytes = rows * j.m;
@@ -330,6 +380,8 @@ int run_job(DevCtx* c, const Job& j) {
         par_memcpy(s.h_in, src, bytes);
       src = s.h_in;
     }
+    if (trace.path) trace.bytes[ci] = bytes;
+    trace.mark(ci, 0, s.stream);
     GAES_CK(cudaMemcpyAsync(s.d_in, src, bytes, cudaMemcpyHostToDevice, s.stream));
     Job shared_view;
     const Job* jc = &j;
@@ -348,11 +400,13 @@ int run_job(DevCtx* c, const Job& j) {
       }
       GAES_CK(cudaMemcpyAsync(s.d_iv, ivsrc, rows * 16, cudaMemcpyHostToDevice, s.stream));
     }
+    trace.mark(ci, 1, s.stream);
     const bool iv_tex = jc->ivs && jc->mode == Mode::kChain && j.m == 16;
     int rc = launch_chunk(c, lane, *jc, s.stream, s.d_in, s.d_out, s.d_iv, r0, rows, compact,
                           tex_for(c, s.d_in, s.cap, s.stream),
                           iv_tex ? tex_for(c, s.d_iv, s.iv_cap, s.stream) : TexLease());
     if (rc) return rc;
+    trace.mark(ci, 2, s.stream);
     if (out_pinned) {
       GAES_CK(cudaMemcpyAsync(j.out + off, s.d_out, bytes, cudaMemcpyDeviceToHost, s.stream));
     } else {
@@ -360,7 +414,9 @@ int run_job(DevCtx* c, const Job& j) {
       s.pending_dst = j.out + off;
       s.pending_bytes = bytes;
     }
+    trace.mark(ci, 3, s.stream);
     GAES_CK(cudaEventRecord(s.done, s.stream));
+    trace.host_mark(ci, 2);
   }
   // drain in issue order
   for (size_t ci = (nchunks > (size_t)kSlots ? nchunks - kSlots : 0); ci < nchunks; ci++) {

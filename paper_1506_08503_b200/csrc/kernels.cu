@@ -675,7 +675,11 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const bool pdl = [] {
+    const char* e = std::getenv("GAES_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
