@@ -319,21 +319,30 @@ static constexpr int kRowsTmaTileBytes = 32 * 32;       // 32 rows x 32 bytes
 static constexpr int kRowsTmaWarpBytes = 3 * kRowsTmaTileBytes;  // 2 load buffers + 1 store buffer
 static constexpr int kTablesBytes = 2 * kRegionBytes;   // T0|T1, T2|T3
 
-__global__ void __launch_bounds__(kBlockThreads, 1)
+// 28 warps at most: with the 1024-thread bound (64-register cap) ptxas keeps
+// the shared-window base in a regular register and adds it to every table
+// address (one extra IMAD per lookup, 144 per block, in an issue-bound
+// kernel); at 896 it folds the base into LDS [R+UR+imm] like the other kernels.
+static constexpr int kRowsTmaMaxWarps = 28;
+
+__global__ void __launch_bounds__(kRowsTmaMaxWarps * 32, 1)
     k_cbc_enc_rows_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
                        uint64_t n_rows, uint64_t bpr, const uint32_t* __restrict__ compact,
                        const __grid_constant__ RoundKeys rk, const uint4* __restrict__ ivs, cudaTextureObject_t tsb) {
   extern __shared__ __align__(1024) char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
-  char* buf = smem + kTablesBytes + warp * kRowsTmaWarpBytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kTablesBytes + nwarps * kRowsTmaWarpBytes) + 2 * warp;
+  // tiles and barriers by shared-space address only (see tma.cuh: keeps the
+  // table lookups at one PRMT + LDS [R+UR+imm] each)
+  const uint32_t buf = smem_addr(smem) + kTablesBytes + warp * kRowsTmaWarpBytes;
+  const uint32_t bar0 = smem_addr(smem) + kTablesBytes + nwarps * kRowsTmaWarpBytes + 16 * warp;
+  const uint32_t bar1 = bar0 + 8;
   // The table fill stages the compact tables in the S region, which this
   // kernel reuses for its tiles and barriers: initialise the barriers after it.
   pdl_prologue(smem, compact, false);  // T tables only; ends with __syncthreads
   if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    mbar_init_s(bar0, 1);
+    mbar_init_s(bar1, 1);
     mbar_init_fence();
   }
   __syncwarp();
@@ -354,44 +363,45 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
     uint4 c = make_uint4(rk.iv[0], rk.iv[1], rk.iv[2], rk.iv[3]);
     if (ivs && row < n_rows) c = __ldg(ivs + row);
     if (lane == 0) {
-      mbar_expect_tx(&bar[0], kRowsTmaTileBytes);
-      tma_load_2d(buf, &tin, 0, r0, &bar[0]);
+      mbar_expect_tx_s(bar0, kRowsTmaTileBytes);
+      tma_load_2d_s(buf, &tin, 0, r0, bar0);
       if (pairs > 1) {
-        mbar_expect_tx(&bar[1], kRowsTmaTileBytes);
-        tma_load_2d(buf + kRowsTmaTileBytes, &tin, 32, r0, &bar[1]);
+        mbar_expect_tx_s(bar1, kRowsTmaTileBytes);
+        tma_load_2d_s(buf + kRowsTmaTileBytes, &tin, 32, r0, bar1);
       }
     }
     for (uint64_t q = 0; q < pairs; q++) {
       const int b = (int)(q & 1);
-      char* tile = buf + b * kRowsTmaTileBytes;
+      const uint32_t tile = buf + b * kRowsTmaTileBytes;
+      const uint32_t bar = b ? bar1 : bar0;
       if (b == 0) {
-        mbar_wait(&bar[0], phase0);
+        mbar_wait_s(bar0, phase0);
         phase0 ^= 1;
       } else {
-        mbar_wait(&bar[1], phase1);
+        mbar_wait_s(bar1, phase1);
         phase1 ^= 1;
       }
-      const uint4 p0 = *reinterpret_cast<const uint4*>(tile + o0);
-      const uint4 p1 = *reinterpret_cast<const uint4*>(tile + o1);
+      const uint4 p0 = lds128_s(tile + o0);
+      const uint4 p1 = lds128_s(tile + o1);
       __syncwarp();
       if (lane == 0 && q + 2 < pairs) {  // refill this buffer two steps ahead
-        mbar_expect_tx(&bar[b], kRowsTmaTileBytes);
-        tma_load_2d(tile, &tin, (int)((q + 2) * 32), r0, &bar[b]);
+        mbar_expect_tx_s(bar, kRowsTmaTileBytes);
+        tma_load_2d_s(tile, &tin, (int)((q + 2) * 32), r0, bar);
       }
       uint4 c0 = c;
       enc(p0, c0);
       uint4 c1 = c0;
       enc(p1, c1);
       c = c1;
-      char* st = buf + 2 * kRowsTmaTileBytes;
+      const uint32_t st = buf + 2 * kRowsTmaTileBytes;
       if (lane == 0) bulk_wait_read<0>();  // the previous store has read the staging tile
       __syncwarp();
-      *reinterpret_cast<uint4*>(st + o0) = c0;
-      *reinterpret_cast<uint4*>(st + o1) = c1;
+      sts128_s(st + o0, c0);
+      sts128_s(st + o1, c1);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(&tout, (int)(q * 32), r0, st);
+        tma_store_2d_s(&tout, (int)(q * 32), r0, st);
         bulk_commit();
       }
     }
@@ -843,14 +853,14 @@ static cudaError_t launch_cbc_enc_rows_tma(const void* in, void* out, uint64_t n
   CUtensorMap tmi, tmo;
   if (!rows_tensor_map(&tmi, in, n_rows, m) || !rows_tensor_map(&tmo, out, n_rows, m)) return cudaSuccess;
   // whole waves of 32-row groups (see rows_geometry): warps per CTA <= 32
-  const uint64_t cap = (uint64_t)sms * 32;
+  const uint64_t cap = (uint64_t)sms * kRowsTmaMaxWarps;
   const uint64_t waves = (groups + cap - 1) / cap;
   const uint64_t per_wave = (groups + waves - 1) / waves;
-  const int warps = (int)std::min<uint64_t>(32, std::max<uint64_t>(4, (per_wave + sms - 1) / sms));
+  const int warps = (int)std::min<uint64_t>(kRowsTmaMaxWarps, std::max<uint64_t>(4, (per_wave + sms - 1) / sms));
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(sms, (per_wave + warps - 1) / warps));
   const size_t smem = kTablesBytes + (size_t)warps * kRowsTmaWarpBytes + (size_t)warps * 16;
   // per (kernel, device), like every other 192 KiB+ kernel
-  if (set_smem(k_cbc_enc_rows_tma, kTablesBytes + 32 * kRowsTmaWarpBytes + 32 * 16) != cudaSuccess) {
+  if (set_smem(k_cbc_enc_rows_tma, kTablesBytes + kRowsTmaMaxWarps * (kRowsTmaWarpBytes + 16)) != cudaSuccess) {
     cudaGetLastError();
     return cudaSuccess;  // fall back to the LDG/STG kernel
   }
