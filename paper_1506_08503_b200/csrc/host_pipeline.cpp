@@ -155,7 +155,7 @@ bool stage_and_check_iv(uint8_t* dst, const uint8_t* src, size_t m, const uint8_
   std::memcpy(&a0, iv0, 8);
   std::memcpy(&a1, iv0 + 8, 8);
   parallel_ranges(rows, std::max<size_t>(1, ((size_t)128 << 10) / m), [&](size_t lo, size_t hi) {
-    std::memcpy(dst + lo * m, src + lo * m, (hi - lo) * m);
+    stage_copy(dst + lo * m, src + lo * m, (hi - lo) * m);
     if (!same.load(std::memory_order_relaxed)) return;
     uint64_t diff = 0;
     for (size_t i = lo; i < hi; i++) {

@@ -15,6 +15,9 @@
 #include <mutex>
 #include <thread>
 #include <vector>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 namespace gaes {
 namespace host {
@@ -165,13 +168,67 @@ void parallel_ranges(size_t n, size_t min_per_thread, F&& fn) {
   if (!host_pool().try_run(want, part)) fn(0, n);
 }
 
+// Copy with non-temporal (streaming) stores: the destination lines are
+// written without first being read into the cache (no read-for-ownership),
+// which on a staging copy saves one of the host-DRAM crossings that bound the
+// pageable drop-in path (the pinned staging buffer is read next by the DMA
+// engine, the caller's output buffer is not re-read by this call).  glibc's
+// memcpy only streams above a size threshold far larger than the per-thread
+// pieces here.  Ends with sfence: the stores are weakly ordered and must be
+// globally visible before the DMA that reads them is issued.
+#if defined(__x86_64__)
+__attribute__((target("avx2"))) inline void nt_copy_avx2(uint8_t* dst, const uint8_t* src, size_t n) {
+  const size_t head = std::min(n, (size_t)((32 - (reinterpret_cast<uintptr_t>(dst) & 31)) & 31));
+  std::memcpy(dst, src, head);
+  dst += head;
+  src += head;
+  n -= head;
+  size_t i = 0;
+  for (; i + 128 <= n; i += 128) {
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 32));
+    const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 64));
+    const __m256i d = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 96));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), a);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 32), b);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 64), c);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 96), d);
+  }
+  std::memcpy(dst + i, src + i, n - i);
+  _mm_sfence();
+}
+#endif
+
+inline bool nt_copies() {
+#if defined(__x86_64__)
+  static const bool on = [] {
+    const char* e = std::getenv("GAES_NT");
+    return !(e && e[0] == '0') && __builtin_cpu_supports("avx2");
+  }();
+  return on;
+#else
+  return false;
+#endif
+}
+
+// Single-threaded piece of a staging copy (streaming stores when available).
+inline void stage_copy(void* dst, const void* src, size_t bytes) {
+#if defined(__x86_64__)
+  if (nt_copies() && bytes >= 4096) {
+    nt_copy_avx2(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), bytes);
+    return;
+  }
+#endif
+  std::memcpy(dst, src, bytes);
+}
+
 inline void par_memcpy(void* dst, const void* src, size_t bytes) {
   static const size_t grain = [] {
     const char* e = std::getenv("GAES_MEMCPY_GRAIN_KB");
     return (size_t)std::max(16, (e && *e) ? std::atoi(e) : 128) << 10;
   }();
   parallel_ranges(bytes, grain, [&](size_t lo, size_t hi) {
-    std::memcpy((uint8_t*)dst + lo, (const uint8_t*)src + lo, hi - lo);
+    stage_copy((uint8_t*)dst + lo, (const uint8_t*)src + lo, hi - lo);
   });
 }
 

@@ -13,7 +13,7 @@ rng = np.random.default_rng(1)
 rk = rng.integers(0, 256, (11, 16), dtype=np.uint8)
 tables = (rk,) + backend_cuda.standard_tables(False)
 iv = rng.integers(0, 256, 16, dtype=np.uint8)
-for lg in (10, 12, 14, 16, 18, 20, 22):
+for lg in [int(a) for a in sys.argv[1:]] or (10, 12, 14, 16, 18, 20, 22):
     n = 1 << lg
     p = rng.integers(0, 256, (n, 16), dtype=np.uint8)
     ivrows = np.tile(iv, (n, 1))
