@@ -840,13 +840,14 @@ static cudaError_t launch_cbc_enc_rows_tma(const void* in, void* out, uint64_t n
   if (!enabled || !tsb || bpr < 8 || (bpr & 1) || n_rows < 32 || n_rows > 0x7FFFFFF0ull || m > 0x7FFFFFF0ull ||
       ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15))
     return cudaSuccess;
-  // The double-buffered TMA pipeline needs many warps per SM to cover the
-  // load latency: with fewer than ~24 row groups per SM (long rows, few of
-  // them) the LDG/STG kernel is faster (2^16 rows of 256 blocks: 642 vs
-  // 669 GB/s; 2^18 rows of 64 blocks: 782 vs 719).
+  // The double-buffered TMA pipeline needs enough warps per SM to cover the
+  // load latency: below ~8 row groups of 32 per SM (long rows, few of them)
+  // the LDG/STG kernel is as fast or faster (scripts/exp/rows_threshold.sh,
+  // 2^24 blocks: 13.8 groups/SM -- 2^16 rows of 256 blocks -- 709 vs 671 GB/s
+  // TMA vs LDG; 6.9 groups/SM 540 vs 543; 3.5 groups/SM 342 vs 361).
   static const uint64_t min_groups_per_sm = [] {
     const char* e = std::getenv("GAES_ROWS_TMA_MIN_GROUPS");  // per SM; tests set 0
-    return (uint64_t)((e && *e) ? std::max(0, std::atoi(e)) : 24);
+    return (uint64_t)((e && *e) ? std::max(0, std::atoi(e)) : 8);
   }();
   const uint64_t groups = (n_rows + 31) / 32;
   if (groups < (uint64_t)sms * min_groups_per_sm) return cudaSuccess;

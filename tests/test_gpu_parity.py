@@ -1073,7 +1073,7 @@ def test_row_cbc_tma_path_matches_oracle(oracle, blocks):
 
 def test_row_cbc_tma_kernel_at_any_row_count():
     """The TMA row kernel itself (forced for every row count with
-    GAES_ROWS_TMA_MIN_GROUPS=0, normally only used from 24 row groups per
+    GAES_ROWS_TMA_MIN_GROUPS=0, normally only used from 8 row groups per
     SM): 1..4 warps with rows, ragged groups, 8..64-block rows."""
     import subprocess
     import sys
