@@ -1099,3 +1099,42 @@ print("ok")
     if "k_cbc_enc_rows\n" in r.stderr or _lib.lib().gaes_uses_sbox_texture(0) != 1:
         pytest.skip("texture S-box unavailable: the TMA row kernel does not apply")
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def _misaligned(shape, offset, rng=None):
+    """A C-contiguous uint8 array whose data starts `offset` bytes past a
+    64-byte boundary (pageable numpy memory)."""
+    n = int(np.prod(shape))
+    raw = np.empty(n + 128, np.uint8)
+    base = (-raw.ctypes.data) % 64
+    a = raw[base + offset: base + offset + n].reshape(shape)
+    if rng is not None:
+        a[...] = rng.integers(0, 256, shape, dtype=np.uint8)
+    return a
+
+
+@pytest.mark.parametrize("m,shared,offset", [(16, True, 1), (16, False, 3), (64, True, 17), (64, False, 8)])
+def test_pageable_dropin_misaligned_multichunk(oracle, m, shared, offset):
+    """The 7-argument drop-in with pageable buffers at odd byte offsets and
+    several staging chunks (40 MiB; pageable chunks are 16 MiB): the
+    streaming-store staging copies handle unaligned heads/tails and every
+    chunk boundary.  Rows are independent, so a row sample is compared with
+    the oracle, and the whole grid round-trips through decrypt."""
+    rng = np.random.default_rng(20 + m + offset)
+    key = rng.bytes(16)
+    n = (40 << 20) // m
+    p = _misaligned((n, m), offset, rng)
+    if shared:
+        ivrows = np.tile(rng.integers(0, 256, 16, dtype=np.uint8), (n, 1))
+    else:
+        ivrows = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    c = _misaligned((n, m), (offset * 7) % 64)
+    backend_cuda.cbc_encrypt(p, ivrows, *oracle.encrypt_tables(key), c)
+    rows = np.unique(np.concatenate([np.arange(8), n - 1 - np.arange(8), rng.choice(n, 512, replace=False),
+                                     np.arange(16 << 20, (16 << 20) + 4 * m, m) // m]))
+    rows = rows[rows < n]
+    want = oracle.encrypt(key, ivrows[rows], np.ascontiguousarray(p[rows]))
+    assert np.array_equal(c[rows], want)
+    back = _misaligned((n, m), (offset * 3) % 64)
+    backend_cuda.cbc_decrypt(c, ivrows, *oracle.decrypt_tables(key), back)
+    assert np.array_equal(back, p)
