@@ -76,6 +76,26 @@ def test_encrypt_decrypt_batch_identical(gaes, n, width, shared):
     assert np.array_equal(pt_gpu, data) and np.array_equal(pt_ref, data)
 
 
+def test_vectorised_batches_through_reference_entry_points(gaes):
+    """paper_1506_08503_b200.batch builds the reference's MessageBatch without
+    its per-message loop; the unchanged encrypt_batch / decrypt_batch take it
+    on the cuda backend and agree with the compiled backend on a
+    reference-built batch."""
+    from paper_1506_08503_b200 import batch as B
+    rng = np.random.default_rng(44)
+    msgs = [rng.integers(0, 256, int(k), dtype=np.uint8).tobytes() for k in rng.integers(1, 70, 3000)]
+    key, iv = rng.bytes(16), rng.bytes(16)
+    ref_batch, our_batch = gaes.pad_zero(msgs), B.pad_zero(msgs)
+    assert type(our_batch) is type(ref_batch) and our_batch.original_lens == ref_batch.original_lens
+    assert np.array_equal(our_batch.data, ref_batch.data)
+    again = B.message_batch(our_batch.data, our_batch.original_lens)
+    ct_ref, _ = _both(gaes, lambda: gaes.encrypt_batch(key, gaes.IVSet.shared(iv), ref_batch))
+    _, ct_gpu = _both(gaes, lambda: gaes.encrypt_batch(key, gaes.IVSet.shared(iv), again))
+    assert np.array_equal(ct_ref, ct_gpu)
+    _, pt_gpu = _both(gaes, lambda: gaes.decrypt_batch(key, gaes.IVSet.shared(iv), ct_gpu))
+    assert np.array_equal(pt_gpu, ref_batch.data)
+
+
 @pytest.mark.parametrize("workers", [1, 2, 3, 4, 7, 8])
 def test_parallel_entry_points_worker_independent(gaes, workers):
     rng = np.random.default_rng(workers)
