@@ -573,8 +573,8 @@ def roofline_for(args, n, ms_local, clocks, dev, local, step, launches):
                          "l1tex__throughput 98 % (profiles/r1_final_ttable_ncu_summary.md).  Per 32 blocks the L1 "
                          "data banks serve 144 lookup wavefronts + ~11.5 cycles taken by the texture fetches "
                          "(counted by ncu as shared-load bank conflicts in a conflict-free layout) + 4 input line "
-                         "fills + 4 store wavefronts, so the lookups alone cannot exceed ~88 % of the LDS peak "
-                         "at full L1 throughput" if tex_sbox else
+                         "fills + 4 store wavefronts (~164 cycles, an ncu-derived estimate): at full L1 throughput "
+                         "the lookups alone get roughly 88-90 % of the LDS peak" if tex_sbox else
                          "ncu: L1 LSU data pipe 96 % busy"),
         "peak_source": ("measured: gaes_probe_lds_peak (k_lds_peak, conflict-free LDS.32 stream on every lane, "
                         f"{sms} SMs x 1024 threads) in this run; MEASURED_PEAKS.json has no shared-memory figure"
