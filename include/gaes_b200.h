@@ -209,6 +209,18 @@ GAES_API int gaes_uses_sbox_texture(int device);
  * 1 = T-table in shared memory, 2 = bitsliced.  Returns the value set or
  * GAES_EINVAL if the variant is not built. */
 GAES_API int gaes_set_variant(int variant);
+/* Host-runtime counters (tests / measurement; no reference counterpart).
+ * Fills out[0..n) with, in order: copy pools created, parallel copy regions
+ * run, most regions ever running at once, regions run on the caller's thread
+ * because the pool was busy, texture objects created on the current device,
+ * texture-cache entries on the current device, keys expanded by host
+ * many-key jobs, shard runner threads (all devices).  Returns the number of
+ * counters written. */
+GAES_API int gaes_debug_counters(int64_t *out, int n);
+/* Self-test of the host copy pool (no GPU needed): `regions` back-to-back
+ * parallel regions of `parts` parts on a private pool of `workers` threads;
+ * returns how many parts ran other than exactly once (0 = correct). */
+GAES_API int64_t gaes_host_pool_selftest(int regions, int parts, int workers);
 
 #ifdef __cplusplus
 }

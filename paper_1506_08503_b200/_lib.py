@@ -54,6 +54,8 @@ SIGNATURES = {
     "gaes_probe_round_rate": (_i, [_i, ctypes.c_uint32, _vp, _vp]),
     "gaes_probe_lds_peak": (_i, [_i, ctypes.c_uint32, _vp, _vp]),
     "gaes_uses_sbox_texture": (_i, [_i]),
+    "gaes_debug_counters": (_i, [_vp, _i]),
+    "gaes_host_pool_selftest": (ctypes.c_int64, [_i, _i, _i]),
 }
 
 
@@ -100,3 +102,14 @@ def last_kernel() -> str:
 
 def set_num_gpus(n: int) -> int:
     return int(lib().gaes_set_num_gpus(int(n)))
+
+
+DEBUG_COUNTERS = ("pools", "regions", "max_concurrent_regions", "busy_fallbacks", "textures_created",
+                  "textures_cached", "keys_expanded", "shard_runner_threads")
+
+
+def debug_counters() -> dict:
+    """gaes_debug_counters() as a dict (names: DEBUG_COUNTERS)."""
+    buf = (ctypes.c_int64 * len(DEBUG_COUNTERS))()
+    k = check(lib().gaes_debug_counters(ctypes.addressof(buf), len(DEBUG_COUNTERS)))
+    return {name: int(buf[i]) for i, name in enumerate(DEBUG_COUNTERS[:k])}

@@ -24,6 +24,31 @@ def _message_batch_cls():
     return MessageBatch
 
 
+# The constructor bypass below is only valid for the dataclass this module
+# was written against: exactly the two fields of aes_cbc.py:45-52.
+_EXPECTED_FIELDS = ("data", "original_lens")
+
+
+def bypass_ok(cls) -> bool:
+    """True when `cls` is a dataclass with exactly (data, original_lens): then
+    a validated batch can be built without re-running its per-message
+    __post_init__ loop.  Any other shape (a field added upstream, a plain
+    class) goes through the real constructor."""
+    import dataclasses
+    if not dataclasses.is_dataclass(cls):
+        return False
+    return tuple(f.name for f in dataclasses.fields(cls)) == _EXPECTED_FIELDS
+
+
+def _build(cls, data: np.ndarray, lens: tuple):
+    if not bypass_ok(cls):
+        return cls(data=data, original_lens=lens)  # the real constructor (and its checks)
+    batch = object.__new__(cls)  # fields already validated: skip the per-message loop
+    object.__setattr__(batch, "data", data)
+    object.__setattr__(batch, "original_lens", lens)
+    return batch
+
+
 def gather_rows(buf: np.ndarray, starts: np.ndarray, lens: np.ndarray, width: int) -> np.ndarray:
     """u8[N, width] grid whose row i is buf[starts[i] : starts[i] + lens[i]]
     followed by zeros: each row's `width` bytes are gathered from its start
@@ -89,10 +114,7 @@ def message_batch(data, original_lens, cls=None):
         raise ValueError(f"message {i} has invalid length {lens_t[i]}")
     if why == "padding":
         raise ValueError(f"message {i} has nonzero padding bytes")
-    batch = object.__new__(cls)  # fields already validated: skip the per-message loop
-    object.__setattr__(batch, "data", data)
-    object.__setattr__(batch, "original_lens", lens_t)
-    return batch
+    return _build(cls, data, lens_t)
 
 
 def pad_zero(messages, cls=None):
@@ -110,7 +132,4 @@ def pad_zero(messages, cls=None):
     starts = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
     grid = gather_rows(buf, starts, lens, width)
     cls = cls or _message_batch_cls()
-    batch = object.__new__(cls)  # lengths positive and padding zero by construction
-    object.__setattr__(batch, "data", grid)
-    object.__setattr__(batch, "original_lens", tuple(lens.tolist()))
-    return batch
+    return _build(cls, grid, tuple(lens.tolist()))  # lengths positive and padding zero by construction

@@ -4,8 +4,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/gaes_b200.h"
 #include "device_ctx.h"
@@ -42,6 +45,48 @@ GAES_API const char* gaes_last_kernel(void) {
   std::lock_guard<std::mutex> lk(g_name_mu);
   copy = g_last_kernel;
   return copy.c_str();
+}
+
+GAES_API int gaes_debug_counters(int64_t* out, int n) {
+  if (!out || n < 0) return fail(GAES_EINVAL, "null counter buffer");
+  host::PoolStats& st = host::pool_stats();
+  int64_t tex_created = 0, tex_cached = 0, runners = 0;
+  DevCtx* c = nullptr;
+  if (device_count() > 0 && current_ctx(&c) == GAES_OK) {
+    std::lock_guard<std::mutex> lk(c->tex_mu);
+    tex_created = (int64_t)c->tex_created;
+    tex_cached = (int64_t)c->tex_cache.size();
+  }
+  for (int d = 0; d < std::max(0, device_count()); d++) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    if (g_ctx[d]) runners += g_ctx[d]->runner.threads();
+  }
+  const int64_t v[] = {st.pools.load(), st.regions.load(), st.max_active.load(), st.busy_fallbacks.load(),
+                       tex_created, tex_cached, g_keys_expanded.load(), runners};
+  const int k = std::min<int>(n, (int)(sizeof(v) / sizeof(v[0])));
+  for (int i = 0; i < k; i++) out[i] = v[i];
+  return k;
+}
+
+GAES_API int64_t gaes_host_pool_selftest(int regions, int parts, int workers) {
+  if (regions < 0 || parts <= 0 || workers < 0) return fail(GAES_EINVAL, "bad self-test arguments");
+  // A private pool hammered with back-to-back regions of `parts` parts; every
+  // part of every region must run exactly once (a part claimed twice, or
+  // never, is an error).  Returns the number of violations.
+  host::HostPool pool(workers);
+  std::vector<std::atomic<int>> hits((size_t)parts);
+  int64_t bad = 0;
+  for (int r = 0; r < regions; r++) {
+    for (auto& h : hits) h.store(0, std::memory_order_relaxed);
+    const std::function<void(size_t)> fn = [&](size_t i) {
+      hits[i].fetch_add(1, std::memory_order_relaxed);
+      if ((i & 7) == 0) std::this_thread::yield();  // widen the windows a stale claimant could use
+    };
+    while (!pool.try_run((size_t)parts, fn)) {
+    }
+    for (auto& h : hits) bad += h.load() != 1;
+  }
+  return bad;
 }
 
 GAES_API int gaes_set_variant(int variant) {
@@ -228,15 +273,19 @@ GAES_API int gaes_encrypt_blocks_dev(const void* in, void* out, size_t n_blocks,
   if (rc) return rc;
   const RoundKeys k = make_enc_keys(round_keys, iv, true);
   const void* src = nullptr;
+  void* dst = nullptr;
   PrivateInput tmp;
+  PrivateOutput tmpo;
   rc = private_input_if_aliased(in, out, n_blocks * 16, false, (cudaStream_t)stream, &src, &tmp);
+  if (!rc) rc = aligned_output(out, n_blocks * 16, (cudaStream_t)stream, &dst, &tmpo);
   if (rc) return rc;
-  return for_segments(c, n_blocks, [&](size_t off, size_t cnt) {
+  rc = for_segments(c, n_blocks, [&](size_t off, size_t cnt) {
     const uint4* i = static_cast<const uint4*>(src) + off;
-    GAES_CK(launch_enc_folded(c, i, static_cast<uint4*>(out) + off, cnt, c->d_std_enc, k, ilp_default(),
+    GAES_CK(launch_enc_folded(c, i, static_cast<uint4*>(dst) + off, cnt, c->d_std_enc, k, ilp_default(),
                               (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream)));
     return GAES_OK;
   });
+  return rc ? rc : tmpo.finish();
 }
 
 GAES_API int gaes_decrypt_blocks_dev(const void* in, void* out, size_t n_blocks, const uint8_t round_keys[176],
@@ -248,17 +297,21 @@ GAES_API int gaes_decrypt_blocks_dev(const void* in, void* out, size_t n_blocks,
   if (rc) return rc;
   const RoundKeys k = make_dec_keys(round_keys, iv, true, nullptr);
   const void* src = nullptr;
+  void* dst = nullptr;
   PrivateInput tmp;
+  PrivateOutput tmpo;
   rc = private_input_if_aliased(in, out, n_blocks * 16, false, (cudaStream_t)stream, &src, &tmp);
+  if (!rc) rc = aligned_output(out, n_blocks * 16, (cudaStream_t)stream, &dst, &tmpo);
   if (rc) return rc;
-  return for_segments(c, n_blocks, [&](size_t off, size_t cnt) {
+  rc = for_segments(c, n_blocks, [&](size_t off, size_t cnt) {
     const uint4* i = static_cast<const uint4*>(src) + off;
-    GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), i, static_cast<uint4*>(out) + off, cnt, c->d_std_dec, k,
+    GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), i, static_cast<uint4*>(dst) + off, cnt, c->d_std_dec, k,
                           nullptr, 1, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream), 0,
                           sbox_tex(c, c->d_std_dec)));
     note_kernel("k_blocks_dec_folded");
     return GAES_OK;
   });
+  return rc ? rc : tmpo.finish();
 }
 
 GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m, const void* ivs_dev,
@@ -273,11 +326,15 @@ GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m,
   if (bpr == 1 && !ivs_dev) return gaes_encrypt_blocks_dev(in, out, n, round_keys, iv, stream);
   const RoundKeys k = make_enc_keys(round_keys, iv, false);
   const void* src = nullptr;
-  PrivateInput tmp;
+  void* out_w = nullptr;
+  PrivateInput tmp, tmpiv;
+  PrivateOutput tmpo;
   rc = private_input_if_aliased(in, out, n * m, false, (cudaStream_t)stream, &src, &tmp);
+  if (!rc) rc = aligned_output(out, n * m, (cudaStream_t)stream, &out_w, &tmpo);
+  if (!rc) rc = aligned_input(ivs_dev, n * 16, (cudaStream_t)stream, &ivs_dev, &tmpiv);
   if (rc) return rc;
   if (bpr == 1) {
-    GAES_CK(launch_blocks(false, kIvChain, ilp_default(), src, out, n, c->d_std_enc, k, ivs_dev, 1, c->sms,
+    GAES_CK(launch_blocks(false, kIvChain, ilp_default(), src, out_w, n, c->d_std_enc, k, ivs_dev, 1, c->sms,
                           (cudaStream_t)stream, tex_for(c, src, n * 16, (cudaStream_t)stream),
                           tex_for(c, ivs_dev, n * 16, (cudaStream_t)stream), sbox_tex(c, c->d_std_enc)));
     note_kernel("k_blocks_enc_chain");
@@ -286,7 +343,7 @@ GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m,
     const size_t seg_blocks = tex_segment_blocks(c);
     const size_t seg_rows = seg_blocks >= bpr ? seg_blocks / bpr : n;
     const uint8_t* i8 = static_cast<const uint8_t*>(src);
-    uint8_t* o8 = static_cast<uint8_t*>(out);
+    uint8_t* o8 = static_cast<uint8_t*>(out_w);
     const uint8_t* v8 = static_cast<const uint8_t*>(ivs_dev);
     for (size_t r = 0; r < n; r += seg_rows) {
       const size_t cnt = std::min(seg_rows, n - r);
@@ -296,7 +353,7 @@ GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m,
     }
     note_kernel(last_rows_launch_used_tma() ? "k_cbc_enc_rows_tma" : "k_cbc_enc_rows");
   }
-  return GAES_OK;
+  return tmpo.finish();
 }
 
 GAES_API int gaes_cbc_decrypt_dev(const void* in, void* out, size_t n, size_t m, const void* ivs_dev,
@@ -311,15 +368,19 @@ GAES_API int gaes_cbc_decrypt_dev(const void* in, void* out, size_t n, size_t m,
   if (bpr == 1 && !ivs_dev) return gaes_decrypt_blocks_dev(in, out, n, round_keys, iv, stream);
   const RoundKeys k = make_dec_keys(round_keys, iv, false, nullptr);
   const void* src = nullptr;
-  PrivateInput tmp;
+  void* out_w = nullptr;
+  PrivateInput tmp, tmpiv;
+  PrivateOutput tmpo;
   rc = private_input_if_aliased(in, out, n * m, bpr > 1, (cudaStream_t)stream, &src, &tmp);
+  if (!rc) rc = aligned_output(out, n * m, (cudaStream_t)stream, &out_w, &tmpo);
+  if (!rc) rc = aligned_input(ivs_dev, n * 16, (cudaStream_t)stream, &ivs_dev, &tmpiv);
   if (rc) return rc;
-  GAES_CK(launch_blocks(true, kIvChain, ilp_default(), src, out, n * bpr, c->d_std_dec, k, ivs_dev, bpr, c->sms,
+  GAES_CK(launch_blocks(true, kIvChain, ilp_default(), src, out_w, n * bpr, c->d_std_dec, k, ivs_dev, bpr, c->sms,
                         (cudaStream_t)stream, tex_for(c, src, n * bpr * 16, (cudaStream_t)stream),
                         bpr == 1 && ivs_dev ? tex_for(c, ivs_dev, n * 16, (cudaStream_t)stream) : TexLease(),
                         sbox_tex(c, c->d_std_dec)));
   note_kernel("k_blocks_dec_chain");
-  return GAES_OK;
+  return tmpo.finish();
 }
 
 GAES_API int gaes_expand_keys_dev(const void* keys, size_t k, void* rk_enc, void* rk_dec, void* stream) {
@@ -328,10 +389,18 @@ GAES_API int gaes_expand_keys_dev(const void* keys, size_t k, void* rk_enc, void
   DevCtx* c = nullptr;
   int rc = current_ctx(&c);
   if (rc) return rc;
-  GAES_CK(launch_expand_keys((const uint8_t*)keys, k, c->d_std_enc, (uint8_t*)rk_enc, (uint8_t*)rk_dec,
+  // the schedules are written as 32-bit words: misaligned outputs go through
+  // private buffers
+  void *enc = nullptr, *dec = nullptr;
+  PrivateOutput tenc, tdec;
+  rc = aligned_output(rk_enc, k * 176, (cudaStream_t)stream, &enc, &tenc);
+  if (!rc) rc = aligned_output(rk_dec, k * 176, (cudaStream_t)stream, &dec, &tdec);
+  if (rc) return rc;
+  GAES_CK(launch_expand_keys((const uint8_t*)keys, k, c->d_std_enc, (uint8_t*)enc, (uint8_t*)dec,
                              (cudaStream_t)stream));
   note_kernel("k_expand_keys");
-  return GAES_OK;
+  rc = tenc.finish();
+  return rc ? rc : tdec.finish();
 }
 
 GAES_API int gaes_many_key_encrypt_dev(const void* in, void* out, size_t blocks_per_key, size_t k,
@@ -341,18 +410,24 @@ GAES_API int gaes_many_key_encrypt_dev(const void* in, void* out, size_t blocks_
   DevCtx* c = nullptr;
   int rc = current_ctx(&c);
   if (rc) return rc;
-  const void* src = nullptr;
-  PrivateInput tmp;
+  const void *src = nullptr, *rks = nullptr, *kivs = nullptr;
+  void* dst = nullptr;
+  PrivateInput tmp, trk, tiv;
+  PrivateOutput tmpo;
   rc = private_input_if_aliased(in, out, blocks_per_key * k * 16, false, (cudaStream_t)stream, &src, &tmp);
+  if (!rc) rc = aligned_output(out, blocks_per_key * k * 16, (cudaStream_t)stream, &dst, &tmpo);
+  if (!rc) rc = aligned_input(rk_enc, k * 176, (cudaStream_t)stream, &rks, &trk);
+  if (!rc) rc = aligned_input(ivs_dev, k * 16, (cudaStream_t)stream, &kivs, &tiv);
   if (rc) return rc;
-  return for_segments(c, blocks_per_key * k, [&](size_t off, size_t cnt) {
+  rc = for_segments(c, blocks_per_key * k, [&](size_t off, size_t cnt) {
     const uint4* i = static_cast<const uint4*>(src) + off;
-    GAES_CK(launch_many_key(false, i, static_cast<uint4*>(out) + off, cnt, off, blocks_per_key, c->d_std_enc, rk_enc,
-                            ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream),
+    GAES_CK(launch_many_key(false, i, static_cast<uint4*>(dst) + off, cnt, off, blocks_per_key, c->d_std_enc, rks,
+                            kivs, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream),
                             sbox_tex(c, c->d_std_enc)));
     note_kernel("k_many_key_enc");
     return GAES_OK;
   });
+  return rc ? rc : tmpo.finish();
 }
 
 GAES_API int gaes_many_key_decrypt_dev(const void* in, void* out, size_t blocks_per_key, size_t k,
@@ -362,18 +437,24 @@ GAES_API int gaes_many_key_decrypt_dev(const void* in, void* out, size_t blocks_
   DevCtx* c = nullptr;
   int rc = current_ctx(&c);
   if (rc) return rc;
-  const void* src = nullptr;
-  PrivateInput tmp;
+  const void *src = nullptr, *rks = nullptr, *kivs = nullptr;
+  void* dst = nullptr;
+  PrivateInput tmp, trk, tiv;
+  PrivateOutput tmpo;
   rc = private_input_if_aliased(in, out, blocks_per_key * k * 16, false, (cudaStream_t)stream, &src, &tmp);
+  if (!rc) rc = aligned_output(out, blocks_per_key * k * 16, (cudaStream_t)stream, &dst, &tmpo);
+  if (!rc) rc = aligned_input(rk_dec, k * 176, (cudaStream_t)stream, &rks, &trk);
+  if (!rc) rc = aligned_input(ivs_dev, k * 16, (cudaStream_t)stream, &kivs, &tiv);
   if (rc) return rc;
-  return for_segments(c, blocks_per_key * k, [&](size_t off, size_t cnt) {
+  rc = for_segments(c, blocks_per_key * k, [&](size_t off, size_t cnt) {
     const uint4* i = static_cast<const uint4*>(src) + off;
-    GAES_CK(launch_many_key(true, i, static_cast<uint4*>(out) + off, cnt, off, blocks_per_key, c->d_std_dec, rk_dec,
-                            ivs_dev, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream),
+    GAES_CK(launch_many_key(true, i, static_cast<uint4*>(dst) + off, cnt, off, blocks_per_key, c->d_std_dec, rks,
+                            kivs, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream),
                             sbox_tex(c, c->d_std_dec)));
     note_kernel("k_many_key_dec");
     return GAES_OK;
   });
+  return rc ? rc : tmpo.finish();
 }
 
 }  // extern "C"

@@ -1,7 +1,12 @@
 // device_ctx.cpp -- see device_ctx.h.
 #include "device_ctx.h"
 
+#include <cuda.h>
+#include <sched.h>
+
 #include <algorithm>
+#include <cctype>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -220,14 +225,38 @@ void query_tex_limits(DevCtx* c) {
 }
 
 
+// Identity of the allocation `p` lies in (CU_POINTER_ATTRIBUTE_BUFFER_ID:
+// unique per allocation for the life of the process, so a buffer freed and
+// re-allocated at the same address gets a new id), through the runtime's
+// driver entry point (no libcuda link dependency).  0 if unavailable.
+unsigned long long buffer_id(const void* p) {
+  using GetAttrFn = CUresult (*)(void*, CUpointer_attribute, CUdeviceptr);
+  static GetAttrFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuPointerGetAttribute", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (GetAttrFn) nullptr;
+    }
+    return reinterpret_cast<GetAttrFn>(f);
+  }();
+  unsigned long long id = 0;
+  if (!fn || fn(&id, CU_POINTER_ATTRIBUTE_BUFFER_ID, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return 0;
+  return id;
+}
+
 // A linear uint4 texture over [ptr, ptr + bytes) for the texture-path input
-// loads, cached per device by pointer (callers and the staging slots reuse
-// buffers).  Empty (handle 0) when disabled (GAES_TEXIN=0), misaligned, too
-// large or unavailable -- the kernels then use LDG.  Must be called with
-// c->dev current and the lease used for one launch on `stream`.  At 64
-// entries the least recently used idle entry is evicted after waiting for
-// the launches that read it (its `last` event); entries lent out right now
-// are never evicted.
+// loads, cached per device by (pointer, allocation id): callers and the
+// staging slots reuse buffers, and a buffer freed and re-allocated at the
+// same address is a different allocation, whose old texture object must not
+// be reused (it was created over memory that no longer exists).  Empty
+// (handle 0) when disabled (GAES_TEXIN=0), misaligned, too large or
+// unavailable -- the kernels then use LDG.  Must be called with c->dev
+// current and the lease used for one launch on `stream`.  At 64 entries the
+// least recently used idle entry is evicted after waiting for the launches
+// that read it (its per-stream events); entries lent out right now are never
+// evicted.
 TexLease tex_for(DevCtx* c, const void* ptr, size_t bytes, cudaStream_t stream) {
   static const bool enabled = env_int("GAES_TEXIN", 1) != 0;
   if (!enabled || !ptr || bytes < 16) return {};
@@ -239,16 +268,30 @@ TexLease tex_for(DevCtx* c, const void* ptr, size_t bytes, cudaStream_t stream) 
     return {};
   }
   if (cap != cudaStreamCaptureStatusNone) return {};
+  const unsigned long long id = buffer_id(ptr);
   std::lock_guard<std::mutex> lk(c->tex_mu);
   query_tex_limits(c);
   if (c->tex_align < 0 || reinterpret_cast<uintptr_t>(ptr) % (uintptr_t)c->tex_align != 0) return {};
   if (bytes / 16 > c->tex_max_texels || bytes / 16 > 0x7FFFFFFFull) return {};
-  for (auto& t : c->tex_cache)
-    if (t->ptr == ptr && t->bytes >= bytes) {
+  auto evict = [&](size_t i) {  // users == 0 (checked by the caller, under tex_mu)
+    if (!c->tex_cache[i]->drain()) return false;
+    c->tex_cache.erase(c->tex_cache.begin() + i);
+    return true;
+  };
+  for (size_t i = 0; i < c->tex_cache.size(); i++) {
+    auto& t = c->tex_cache[i];
+    if (t->ptr != ptr) continue;
+    if (t->buffer_id == id && t->bytes >= bytes) {
       t->users.fetch_add(1, std::memory_order_acquire);
       t->stamp = ++c->tex_clock;
       return TexLease(t.get(), stream);
     }
+    // same address, another allocation (or a shorter view): drop the stale entry
+    if (t->buffer_id != id && t->users.load(std::memory_order_acquire) == 0) {
+      if (!evict(i)) return {};
+      break;
+    }
+  }
   if (c->tex_cache.size() >= 64) {
     // users only grows under tex_mu, so an idle entry seen here stays idle
     size_t victim = c->tex_cache.size();
@@ -256,21 +299,9 @@ TexLease tex_for(DevCtx* c, const void* ptr, size_t bytes, cudaStream_t stream) 
       if (c->tex_cache[i]->users.load(std::memory_order_acquire) == 0 &&
           (victim == c->tex_cache.size() || c->tex_cache[i]->stamp < c->tex_cache[victim]->stamp))
         victim = i;
-    if (victim == c->tex_cache.size()) return {};
-    auto& v = c->tex_cache[victim];
-    if (cudaEventSynchronize(v->last) != cudaSuccess) {
-      cudaGetLastError();
-      return {};
-    }
-    cudaDestroyTextureObject(v->tex);
-    cudaEventDestroy(v->last);
-    c->tex_cache.erase(c->tex_cache.begin() + victim);
+    if (victim == c->tex_cache.size() || !evict(victim)) return {};
   }
   auto e = std::make_unique<DevCtx::Tex>();
-  if (cudaEventCreateWithFlags(&e->last, cudaEventDisableTiming) != cudaSuccess) {
-    cudaGetLastError();
-    return {};
-  }
   cudaResourceDesc rd = {};
   rd.resType = cudaResourceTypeLinear;
   rd.res.linear.devPtr = const_cast<void*>(ptr);
@@ -280,14 +311,16 @@ TexLease tex_for(DevCtx* c, const void* ptr, size_t bytes, cudaStream_t stream) 
   td.readMode = cudaReadModeElementType;
   if (cudaCreateTextureObject(&e->tex, &rd, &td, nullptr) != cudaSuccess) {
     cudaGetLastError();
-    cudaEventDestroy(e->last);
+    e->tex = 0;
     return {};
   }
   e->ptr = ptr;
   e->bytes = bytes;
+  e->buffer_id = id;
   e->stamp = ++c->tex_clock;
   e->users.store(1, std::memory_order_relaxed);
   c->tex_cache.push_back(std::move(e));
+  c->tex_created++;
   return TexLease(c->tex_cache.back().get(), stream);
 }
 
@@ -314,7 +347,8 @@ int private_input_if_aliased(const void* in, const void* out, size_t bytes, bool
   *src = in;
   const uintptr_t a = reinterpret_cast<uintptr_t>(in), b = reinterpret_cast<uintptr_t>(out);
   const bool overlap = a < b + bytes && b < a + bytes;
-  if (!overlap || (a == b && !identical_is_unsafe)) return GAES_OK;
+  // a misaligned input is copied too: the kernels load whole 16-byte blocks
+  if (aligned16(in) && (!overlap || (a == b && !identical_is_unsafe && aligned16(out)))) return GAES_OK;
   GAES_CK(cudaMallocAsync(&tmp->ptr, bytes, stream));
   tmp->stream = stream;
   GAES_CK(cudaMemcpyAsync(tmp->ptr, in, bytes, cudaMemcpyDeviceToDevice, stream));
@@ -323,6 +357,71 @@ int private_input_if_aliased(const void* in, const void* out, size_t bytes, bool
 }
 
 
+
+int aligned_input(const void* p, size_t bytes, cudaStream_t stream, const void** src, PrivateInput* tmp) {
+  *src = p;
+  if (!p || aligned16(p) || bytes == 0) return GAES_OK;
+  GAES_CK(cudaMallocAsync(&tmp->ptr, bytes, stream));
+  tmp->stream = stream;
+  GAES_CK(cudaMemcpyAsync(tmp->ptr, p, bytes, cudaMemcpyDeviceToDevice, stream));
+  *src = tmp->ptr;
+  return GAES_OK;
+}
+
+int aligned_output(void* out, size_t bytes, cudaStream_t stream, void** dst, PrivateOutput* tmp) {
+  *dst = out;
+  if (!out || aligned16(out) || bytes == 0) return GAES_OK;
+  GAES_CK(cudaMallocAsync(&tmp->ptr, bytes, stream));
+  tmp->stream = stream;
+  tmp->dst = out;
+  tmp->bytes = bytes;
+  *dst = tmp->ptr;
+  return GAES_OK;
+}
+
+std::vector<int> device_local_cpus(int dev) {
+  std::vector<int> cpus;
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), dev) != cudaSuccess) {
+    cudaGetLastError();
+    return cpus;
+  }
+  std::string id(bus);
+  for (auto& ch : id) ch = (char)std::tolower((unsigned char)ch);
+  FILE* f = std::fopen(("/sys/bus/pci/devices/" + id + "/local_cpulist").c_str(), "r");
+  if (!f) return cpus;
+  char buf[4096] = {0};
+  const size_t got = std::fread(buf, 1, sizeof(buf) - 1, f);
+  std::fclose(f);
+  buf[got] = 0;
+  cpu_set_t allowed;
+  const bool have_mask = sched_getaffinity(0, sizeof(allowed), &allowed) == 0;
+  for (char* p = buf; *p && *p != '\n';) {  // "0-31,64-95"
+    char* end = nullptr;
+    const long lo = std::strtol(p, &end, 10);
+    if (end == p) break;
+    long hi = lo;
+    p = end;
+    if (*p == '-') {
+      hi = std::strtol(p + 1, &end, 10);
+      p = end;
+    }
+    for (long c = lo; c <= hi && c < CPU_SETSIZE; c++)
+      if (!have_mask || CPU_ISSET((int)c, &allowed)) cpus.push_back((int)c);
+    if (*p == ',') p++;
+  }
+  return cpus;
+}
+
+host::HostPool* device_pool(DevCtx* c) {
+  std::call_once(c->pool_once, [c] {
+    // this device's share of the process's copy threads (logical devices
+    // on one node split its CPUs), pinned to the CPUs local to the GPU
+    const int n = std::max(1, host::host_threads() / std::max(1, device_count()));
+    c->pool = new host::HostPool(n - 1, device_local_cpus(c->dev));  // leaked with the context
+  });
+  return c->pool;
+}
 
 int ilp_default() {
   // ILP 1 measured ~1% faster than 2 at configs 2 and 3 (finer tail, 40 regs)

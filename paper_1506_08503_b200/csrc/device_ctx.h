@@ -6,12 +6,16 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
 #include <unordered_map>
 #include <vector>
 
+#include "host_pool.h"
 #include "kernels.h"
 #include "runtime.h"
 #include "types.h"
@@ -49,6 +53,46 @@ struct Lane {
   uint32_t* d_tables = nullptr;  // caller tables built here once the per-device cache is full
 };
 
+// Persistent threads that run one device's shards of in-process multi-GPU
+// host jobs (gaes_set_num_gpus > 1): up to kLanes of them, created on demand
+// and kept for the process, so a sharded call spawns no threads.
+class ShardRunner {
+ public:
+  void post(std::function<void()> f) {
+    std::lock_guard<std::mutex> lk(mu_);
+    q_.push_back(std::move(f));
+    if (idle_ == 0 && threads_ < kLanes) {
+      threads_++;
+      std::thread([this] { loop(); }).detach();  // lives as long as the (never destroyed) context
+    }
+    cv_.notify_one();
+  }
+  int threads() {
+    std::lock_guard<std::mutex> lk(mu_);
+    return threads_;
+  }
+
+ private:
+  void loop() {
+    for (;;) {
+      std::function<void()> f;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        idle_++;
+        cv_.wait(lk, [this] { return !q_.empty(); });
+        idle_--;
+        f = std::move(q_.front());
+        q_.pop_front();
+      }
+      f();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<std::function<void()>> q_;
+  int threads_ = 0, idle_ = 0;
+};
+
 struct DevCtx {
   int dev = 0;
   int sms = 148;
@@ -71,17 +115,61 @@ struct DevCtx {
   struct Tex {
     const void* ptr = nullptr;
     size_t bytes = 0;
+    unsigned long long buffer_id = 0;  // CU_POINTER_ATTRIBUTE_BUFFER_ID of the allocation it views (0: unknown)
     cudaTextureObject_t tex = 0;
-    cudaEvent_t last = nullptr;  // recorded after every launch that reads it
-    std::atomic<int> users{0};   // leases not yet enqueued
+    // One event per stream whose launches read this texture, re-recorded
+    // after each such launch; eviction waits on all of them.  Past
+    // kMaxStreams distinct streams, `overflow` makes eviction wait for the
+    // whole device instead.
+    static constexpr size_t kMaxStreams = 8;
+    std::mutex mu;
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> evs;
+    bool overflow = false;
+    std::atomic<int> users{0};  // leases not yet enqueued
     uint64_t stamp = 0;
+    void record(cudaStream_t s) {
+      std::lock_guard<std::mutex> lk(mu);
+      for (auto& e : evs)
+        if (e.first == s) {
+          cudaEventRecord(e.second, s);
+          return;
+        }
+      cudaEvent_t ev = nullptr;
+      if (evs.size() < kMaxStreams && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
+        cudaEventRecord(ev, s);
+        evs.emplace_back(s, ev);
+      } else {
+        cudaGetLastError();
+        overflow = true;
+      }
+    }
+    // Blocks until every launch that read the texture has finished.
+    bool drain() {
+      std::lock_guard<std::mutex> lk(mu);
+      bool ok = true;
+      for (auto& e : evs) ok &= cudaEventSynchronize(e.second) == cudaSuccess;
+      if (overflow) ok &= cudaDeviceSynchronize() == cudaSuccess;
+      if (!ok) cudaGetLastError();
+      return ok;
+    }
+    ~Tex() {
+      for (auto& e : evs) cudaEventDestroy(e.second);
+      if (tex) cudaDestroyTextureObject(tex);
+    }
   };
   std::mutex tex_mu;
   std::vector<std::unique_ptr<Tex>> tex_cache;
   uint64_t tex_clock = 0;
+  uint64_t tex_created = 0;  // texture objects created over caller / slot buffers (gaes_debug_counters)
   int tex_align = 0;
   size_t tex_max_texels = 0;
   Lane lanes[kLanes];
+  // In-process multi-GPU (gaes_set_num_gpus > 1): this device's own host copy
+  // pool, its threads pinned to the CPUs local to the GPU's PCIe root
+  // (created on first sharded use, see device_pool()), and its shard runners.
+  std::once_flag pool_once;
+  host::HostPool* pool = nullptr;
+  ShardRunner runner;
   // Only runs when initialisation fails (live contexts are never destroyed:
   // freeing after the CUDA runtime has shut down at exit is not allowed).
   ~DevCtx() {
@@ -98,10 +186,6 @@ struct DevCtx {
       }
     }
     for (auto& kv : cache) cudaFree(kv.second);
-    for (auto& t : tex_cache) {
-      cudaDestroyTextureObject(t->tex);
-      if (t->last) cudaEventDestroy(t->last);
-    }
   }
 };
 
@@ -114,8 +198,9 @@ struct DeviceGuard {
 
 // A texture object lent to one launch.  It converts to the handle the
 // launcher takes; when the lease ends -- the end of the full expression that
-// enqueued the launch -- an event is recorded on the launch stream, so the
-// entry can later be evicted once exactly the kernels that read it are done.
+// enqueued the launch -- the entry's event for the launch stream is recorded,
+// so the entry can later be evicted once exactly the kernels that read it,
+// on every stream, are done.
 class TexLease {
  public:
   TexLease() = default;
@@ -124,7 +209,7 @@ class TexLease {
   TexLease& operator=(const TexLease&) = delete;
   ~TexLease() {
     if (!e_) return;
-    cudaEventRecord(e_->last, s_);
+    e_->record(s_);
     e_->users.fetch_sub(1, std::memory_order_release);
   }
   operator cudaTextureObject_t() const { return e_ ? e_->tex : 0; }
@@ -142,6 +227,34 @@ struct PrivateInput {
   }
 };
 
+// A caller output the kernels cannot write directly (not 16-byte aligned:
+// they store whole 16-byte blocks): the launches write a private aligned
+// buffer and finish() copies it to the caller's pointer, stream-ordered.
+struct PrivateOutput {
+  void* ptr = nullptr;
+  void* dst = nullptr;
+  size_t bytes = 0;
+  cudaStream_t stream = nullptr;
+  int finish() {
+    if (ptr) GAES_CK(cudaMemcpyAsync(dst, ptr, bytes, cudaMemcpyDeviceToDevice, stream));
+    return GAES_OK;
+  }
+  ~PrivateOutput() {
+    if (ptr) cudaFreeAsync(ptr, stream);
+  }
+};
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Logical device -> context table (device_ctx.cpp); g_ctx_mu guards it.
+extern std::mutex g_ctx_mu;
+extern std::vector<DevCtx*>& g_ctx;
+
+// The host copy pool of c for sharded jobs (see DevCtx::pool).
+host::HostPool* device_pool(DevCtx* c);
+// CPU ids local to CUDA device `dev` (sysfs local_cpulist of its PCI
+// function) that this process may run on; empty if unknown.
+std::vector<int> device_local_cpus(int dev);
 // Number of logical devices (GAES_DEVICE_MAP-aware), -1 before the first query.
 int device_count();
 // Context of logical device `dev`, created on first use (GF layer built on
@@ -158,6 +271,12 @@ TexLease tex_for(DevCtx* c, const void* ptr, size_t bytes, cudaStream_t stream);
 size_t tex_segment_blocks(DevCtx* c);
 int private_input_if_aliased(const void* in, const void* out, size_t bytes, bool identical_is_unsafe,
                              cudaStream_t stream, const void** src, PrivateInput* tmp);
+// `p` itself if 16-byte aligned (or null), else a stream-ordered aligned copy
+// of its `bytes` (kernels read 16-byte blocks).
+int aligned_input(const void* p, size_t bytes, cudaStream_t stream, const void** src, PrivateInput* tmp);
+// `out` itself if 16-byte aligned, else a private buffer that tmp->finish()
+// copies to `out` after the launches.
+int aligned_output(void* out, size_t bytes, cudaStream_t stream, void** dst, PrivateOutput* tmp);
 int ilp_default();
 // S-box texture matching the compact tables `compact` (standard tables only).
 cudaTextureObject_t sbox_tex(const DevCtx* c, const uint32_t* compact);

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -266,11 +267,17 @@ int run_job(DevCtx* c, const Job& j) {
       compact = t;
     }
   } else {
+    // byte-level tables for k_generic_cbc, on the lane's own stream and
+    // complete before any slot stream launches (the slot streams are
+    // non-blocking: a legacy-stream cudaMemcpy from pageable memory would
+    // not order them)
     uint8_t* sc = lane->d_scratch;
-    GAES_CK(cudaMemcpy(sc, j.box, 256, cudaMemcpyHostToDevice));
-    GAES_CK(cudaMemcpy(sc + 256, j.lut, 4096, cudaMemcpyHostToDevice));
-    GAES_CK(cudaMemcpy(sc + 256 + 4096, j.perm, 16, cudaMemcpyHostToDevice));
-    GAES_CK(cudaMemcpy(sc + 256 + 4096 + 16, j.raw_rk, 176, cudaMemcpyHostToDevice));
+    cudaStream_t s0 = lane->slots[0].stream;
+    GAES_CK(cudaMemcpyAsync(sc, j.box, 256, cudaMemcpyHostToDevice, s0));
+    GAES_CK(cudaMemcpyAsync(sc + 256, j.lut, 4096, cudaMemcpyHostToDevice, s0));
+    GAES_CK(cudaMemcpyAsync(sc + 256 + 4096, j.perm, 16, cudaMemcpyHostToDevice, s0));
+    GAES_CK(cudaMemcpyAsync(sc + 256 + 4096 + 16, j.raw_rk, 176, cudaMemcpyHostToDevice, s0));
+    GAES_CK(cudaStreamSynchronize(s0));
   }
 
   if (j.mode == Mode::kManyKey) {
@@ -293,12 +300,13 @@ int run_job(DevCtx* c, const Job& j) {
     GAES_CK(launch_expand_keys(lane->d_mk, j.n_keys, c->d_std_enc, lane->d_mk + kb,
                                j.dec ? lane->d_mk + kb + j.n_keys * 176 : nullptr, s0));
     note_kernel("k_expand_keys");
+    g_keys_expanded.fetch_add((int64_t)j.n_keys, std::memory_order_relaxed);
     GAES_CK(cudaStreamSynchronize(s0));
   }
 
   const bool in_pinned = is_pinned(j.data);
   const bool out_pinned = is_pinned(j.out);
-  if (!(in_pinned && out_pinned) && j.n * j.m >= ((size_t)256 << 10)) host_pool().warm();
+  if (!(in_pinned && out_pinned) && j.n * j.m >= ((size_t)256 << 10)) current_pool().warm();
   const bool need_iv = j.ivs != nullptr;
   const bool iv_pinned = need_iv && is_pinned(j.ivs);
 
@@ -307,12 +315,16 @@ int run_job(DevCtx* c, const Job& j) {
   // caller's host memory over PCIe itself, no staging copies
   // (scripts/exp/zerocopy_probe.py: 21 vs 15 GB/s at 1 MiB, 34 vs 32 at
   // 16 MiB, 38.6 vs 37.9 at 64 MiB; the staged pipeline leads from 256 MiB).
-  // Not for byte-level generic tables (byte loads over PCIe) nor for
-  // overlapping in/out (the kernels assume distinct buffers).
+  // Not for byte-level generic tables (byte loads over PCIe), overlapping
+  // in/out (the kernels assume distinct buffers) or buffers that are not
+  // 16-byte aligned (the kernels move whole 16-byte blocks; a misaligned
+  // vector access would fault the context) -- those take the staged
+  // pipeline, whose DMA copies accept any alignment.
   const size_t total = j.n * j.m;
   const uintptr_t ia = reinterpret_cast<uintptr_t>(j.data), oa = reinterpret_cast<uintptr_t>(j.out);
-  if (in_pinned && out_pinned && (!need_iv || iv_pinned) && j.mode != Mode::kGeneric && total <= zero_copy_bytes() &&
-      !(ia < oa + total && oa < ia + total)) {
+  const bool aligned = aligned16(j.data) && aligned16(j.out) && (!need_iv || aligned16(j.ivs));
+  if (in_pinned && out_pinned && (!need_iv || iv_pinned) && aligned && j.mode != Mode::kGeneric &&
+      total <= zero_copy_bytes() && !(ia < oa + total && oa < ia + total)) {
     const uint8_t* din = host_dev_view(j.data);
     uint8_t* dout = const_cast<uint8_t*>(host_dev_view(j.out));
     const uint8_t* div = need_iv ? host_dev_view(j.ivs) : nullptr;
@@ -447,7 +459,12 @@ int gpus_in_use() {
   return want;
 }
 
-// Shard rows across devices; one host thread per device when > 1.
+// Shard rows across devices.  One device: the caller's thread and the
+// process pool.  Several: shard 0 on the caller's thread, the others on
+// their device's persistent runner threads; each shard stages through its
+// device's own NUMA-local copy pool, so the shards' host copies run in
+// parallel instead of queueing for one pool.  A many-key shard uploads and
+// expands only the keys its rows use.
 int run_sharded(const Job& j) {
   if (j.n == 0) return GAES_OK;
   const int ndev = device_count();
@@ -468,18 +485,37 @@ int run_sharded(const Job& j) {
     if (j.ivs) s.ivs = j.ivs + chunks[i].first * 16;
     s.first = j.first + chunks[i].first;
     s.n = chunks[i].second - chunks[i].first;
+    if (j.mode == Mode::kManyKey) {  // this shard's keys only (rows are blocks here)
+      const size_t k_lo = s.first / j.bpk, k_hi = (s.first + s.n + j.bpk - 1) / j.bpk;
+      s.mk_keys = j.mk_keys + k_lo * 16;
+      if (j.mk_ivs) s.mk_ivs = j.mk_ivs + k_lo * 16;
+      s.n_keys = k_hi - k_lo;
+      s.first -= k_lo * j.bpk;
+    }
     return s;
   };
   if (chunks.size() == 1) return run_job(ctxs[0], shard_job(0));
   std::vector<int> rcs(chunks.size(), GAES_OK);
   std::vector<std::string> errs(chunks.size());
-  std::vector<std::thread> th;
-  for (size_t i = 0; i < chunks.size(); i++)
-    th.emplace_back([&, i] {
-      rcs[i] = run_job(ctxs[i], shard_job(i));
-      if (rcs[i]) errs[i] = t_err;
+  std::mutex mu;
+  std::condition_variable cv;
+  size_t left = chunks.size() - 1;
+  auto run_one = [&](size_t i) {
+    host::PoolScope scope(device_pool(ctxs[i]));
+    rcs[i] = run_job(ctxs[i], shard_job(i));
+    if (rcs[i]) errs[i] = t_err;
+  };
+  for (size_t i = 1; i < chunks.size(); i++)
+    ctxs[i]->runner.post([&, i] {
+      run_one(i);
+      std::lock_guard<std::mutex> lk(mu);
+      if (--left == 0) cv.notify_all();
     });
-  for (auto& t : th) t.join();
+  run_one(0);
+  {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return left == 0; });
+  }
   for (size_t i = 0; i < chunks.size(); i++)
     if (rcs[i]) return fail(rcs[i], "gpu " + std::to_string(i) + ": " + errs[i]);
   return GAES_OK;

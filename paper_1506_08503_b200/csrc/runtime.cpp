@@ -12,6 +12,7 @@ std::mutex g_name_mu;
 std::string g_last_kernel = "";
 std::atomic<int> g_num_gpus{0};
 std::atomic<int> g_variant{0};
+std::atomic<int64_t> g_keys_expanded{0};
 
 int fail(int code, const std::string& msg) {
   t_err = msg;

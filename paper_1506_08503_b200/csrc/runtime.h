@@ -24,6 +24,7 @@ extern std::mutex g_name_mu;
 extern std::string g_last_kernel;         // gaes_last_kernel()
 extern std::atomic<int> g_num_gpus;       // gaes_set_num_gpus()
 extern std::atomic<int> g_variant;        // gaes_set_variant()
+extern std::atomic<int64_t> g_keys_expanded;  // keys expanded by host many-key jobs (gaes_debug_counters)
 
 // Records msg as this thread's last error and returns code.
 int fail(int code, const std::string& msg);

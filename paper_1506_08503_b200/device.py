@@ -223,10 +223,14 @@ def _many_key(enc: bool, x, rks, ivs, out):
     k = rks.shape[0]
     if tuple(rks.shape[1:]) != (11, 16) or k == 0 or x.shape[0] % k:
         raise ValueError("round_keys must be K x 11 x 16 and N a multiple of K")
+    if rks.device != x.device:
+        raise ValueError("round_keys must be on the input's device")
     if ivs is not None:
         ivs = _u8_cuda(ivs, "ivs", 2)
         if tuple(ivs.shape) != (k, 16):
             raise ValueError("ivs must be K x 16")
+        if ivs.device != x.device:
+            raise ValueError("ivs must be on the input's device")
     bpk = x.shape[0] // k
     fn = _lib.lib().gaes_many_key_encrypt_dev if enc else _lib.lib().gaes_many_key_decrypt_dev
     with _on_device(x.device):

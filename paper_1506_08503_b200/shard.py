@@ -89,6 +89,16 @@ def sum_over_ranks(value: int, device=None) -> int:
     return int(t.item())
 
 
+def gather_objects(obj) -> list:
+    """Every rank's ``obj`` in rank order (``[obj]`` without a process group)."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return [obj]
+    res = [None] * dist.get_world_size()
+    dist.all_gather_object(res, obj)
+    return res
+
+
 def parse_cpulist(text: str) -> list:
     """CPU ids from a sysfs cpulist ("0-3,8,10-11")."""
     cpus = []

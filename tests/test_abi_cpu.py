@@ -167,3 +167,19 @@ def test_device_api_rejects_host_tensors(lib):
                  lambda: device.many_key_encrypt(x, torch.zeros((1, 11, 16), dtype=torch.uint8))):
         with pytest.raises(ValueError):
             call()
+
+
+def test_host_pool_claims_each_part_exactly_once():
+    """The copy pool's part claims carry their region's generation (ADVICE
+    r1): thousands of back-to-back regions on a private pool, every part of
+    every region runs exactly once."""
+    from paper_1506_08503_b200 import _lib
+    for parts, workers in ((1, 1), (3, 2), (7, 3), (64, 5)):
+        assert _lib.lib().gaes_host_pool_selftest(3000, parts, workers) == 0
+
+
+def test_debug_counters_without_a_gpu():
+    from paper_1506_08503_b200 import _lib
+    c = _lib.debug_counters()
+    assert set(c) == set(_lib.DEBUG_COUNTERS)
+    assert all(v >= 0 for v in c.values())

