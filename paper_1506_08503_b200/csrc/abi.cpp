@@ -305,10 +305,8 @@ GAES_API int gaes_decrypt_blocks_dev(const void* in, void* out, size_t n_blocks,
   if (rc) return rc;
   rc = for_segments(c, n_blocks, [&](size_t off, size_t cnt) {
     const uint4* i = static_cast<const uint4*>(src) + off;
-    GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), i, static_cast<uint4*>(dst) + off, cnt, c->d_std_dec, k,
-                          nullptr, 1, c->sms, (cudaStream_t)stream, tex_for(c, i, cnt * 16, (cudaStream_t)stream), 0,
-                          sbox_tex(c, c->d_std_dec)));
-    note_kernel("k_blocks_dec_folded");
+    GAES_CK(launch_folded(c, true, i, static_cast<uint4*>(dst) + off, cnt, c->d_std_dec, k, (cudaStream_t)stream,
+                          tex_for(c, i, cnt * 16, (cudaStream_t)stream)));
     return GAES_OK;
   });
   return rc ? rc : tmpo.finish();

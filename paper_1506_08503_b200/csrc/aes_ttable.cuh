@@ -156,4 +156,72 @@ __device__ __forceinline__ void decrypt_rounds(const char* smem, uint32_t lb, ui
   s0 = o0; s1 = o1; s2 = o2; s3 = o3;
 }
 
+// ---------------------------------------------------------------------------
+// Small-batch formulation (k_blocks_small): only region 0 (T0 | T1, 64 KiB)
+// is filled.  MixColumns' matrices are circulant (aes_cbc.py:118-132:
+// circ(2,3,1,1) and circ(14,11,13,9)), so T_j = rotl(T0, 8j): T2 = rot16(T0)
+// and T3 = rot16(T1), and since rotation is XOR-linear one PRMT per output
+// column covers both: t_c = T0[.] ^ T1[.] ^ rot16(T0[.] ^ T1[.]) ^ rk.  The
+// same 144 conflict-free lookups per block, half the table fill, and the
+// fill comes from the kernel parameters (no global round trip).  Standard
+// tables only (the round-10 S-box is the GF layer's texture).
+__device__ __forceinline__ uint32_t rot16(uint32_t x) { return __byte_perm(x, 0, 0x1032); }
+
+__device__ __forceinline__ void encrypt_rounds_rot(const char* smem, uint32_t lb, uint32_t& s0, uint32_t& s1,
+                                                   uint32_t& s2, uint32_t& s3, const RoundKeys& rk,
+                                                   cudaTextureObject_t tsb) {
+#pragma unroll
+  for (int r = 1; r < 10; r++) {
+    const uint32_t t0 = lds_u32(smem, taddr<0>(s0, lb), kOffT0) ^ lds_u32(smem, taddr<1>(s1, lb), kOffT1) ^
+                        rot16(lds_u32(smem, taddr<2>(s2, lb), kOffT0) ^ lds_u32(smem, taddr<3>(s3, lb), kOffT1)) ^
+                        rk.w[4 * r + 0];
+    const uint32_t t1 = lds_u32(smem, taddr<0>(s1, lb), kOffT0) ^ lds_u32(smem, taddr<1>(s2, lb), kOffT1) ^
+                        rot16(lds_u32(smem, taddr<2>(s3, lb), kOffT0) ^ lds_u32(smem, taddr<3>(s0, lb), kOffT1)) ^
+                        rk.w[4 * r + 1];
+    const uint32_t t2 = lds_u32(smem, taddr<0>(s2, lb), kOffT0) ^ lds_u32(smem, taddr<1>(s3, lb), kOffT1) ^
+                        rot16(lds_u32(smem, taddr<2>(s0, lb), kOffT0) ^ lds_u32(smem, taddr<3>(s1, lb), kOffT1)) ^
+                        rk.w[4 * r + 2];
+    const uint32_t t3 = lds_u32(smem, taddr<0>(s3, lb), kOffT0) ^ lds_u32(smem, taddr<1>(s0, lb), kOffT1) ^
+                        rot16(lds_u32(smem, taddr<2>(s1, lb), kOffT0) ^ lds_u32(smem, taddr<3>(s2, lb), kOffT1)) ^
+                        rk.w[4 * r + 3];
+    s0 = t0; s1 = t1; s2 = t2; s3 = t3;
+  }
+#define GAES_LAST_T(a, b, c, d)                                                                     \
+  ((tex_sbox(tsb, (d) >> 24) * 256u + tex_sbox(tsb, ((c) >> 16) & 0xFF)) * 65536u +                 \
+   (tex_sbox(tsb, ((b) >> 8) & 0xFF) * 256u + tex_sbox(tsb, (a) & 0xFF)))
+  const uint32_t o0 = GAES_LAST_T(s0, s1, s2, s3) ^ rk.w[40];
+  const uint32_t o1 = GAES_LAST_T(s1, s2, s3, s0) ^ rk.w[41];
+  const uint32_t o2 = GAES_LAST_T(s2, s3, s0, s1) ^ rk.w[42];
+  const uint32_t o3 = GAES_LAST_T(s3, s0, s1, s2) ^ rk.w[43];
+  s0 = o0; s1 = o1; s2 = o2; s3 = o3;
+}
+
+// Equivalent inverse cipher with Td_j = rotl(Td0, 8j); source word (c - j) mod 4.
+__device__ __forceinline__ void decrypt_rounds_rot(const char* smem, uint32_t lb, uint32_t& s0, uint32_t& s1,
+                                                   uint32_t& s2, uint32_t& s3, const RoundKeys& rk,
+                                                   cudaTextureObject_t tsb) {
+#pragma unroll
+  for (int r = 9; r >= 1; r--) {
+    const uint32_t t0 = lds_u32(smem, taddr<0>(s0, lb), kOffT0) ^ lds_u32(smem, taddr<1>(s3, lb), kOffT1) ^
+                        rot16(lds_u32(smem, taddr<2>(s2, lb), kOffT0) ^ lds_u32(smem, taddr<3>(s1, lb), kOffT1)) ^
+                        rk.w[4 * r + 0];
+    const uint32_t t1 = lds_u32(smem, taddr<0>(s1, lb), kOffT0) ^ lds_u32(smem, taddr<1>(s0, lb), kOffT1) ^
+                        rot16(lds_u32(smem, taddr<2>(s3, lb), kOffT0) ^ lds_u32(smem, taddr<3>(s2, lb), kOffT1)) ^
+                        rk.w[4 * r + 1];
+    const uint32_t t2 = lds_u32(smem, taddr<0>(s2, lb), kOffT0) ^ lds_u32(smem, taddr<1>(s1, lb), kOffT1) ^
+                        rot16(lds_u32(smem, taddr<2>(s0, lb), kOffT0) ^ lds_u32(smem, taddr<3>(s3, lb), kOffT1)) ^
+                        rk.w[4 * r + 2];
+    const uint32_t t3 = lds_u32(smem, taddr<0>(s3, lb), kOffT0) ^ lds_u32(smem, taddr<1>(s2, lb), kOffT1) ^
+                        rot16(lds_u32(smem, taddr<2>(s1, lb), kOffT0) ^ lds_u32(smem, taddr<3>(s0, lb), kOffT1)) ^
+                        rk.w[4 * r + 3];
+    s0 = t0; s1 = t1; s2 = t2; s3 = t3;
+  }
+  const uint32_t o0 = GAES_LAST_T(s0, s3, s2, s1);
+  const uint32_t o1 = GAES_LAST_T(s1, s0, s3, s2);
+  const uint32_t o2 = GAES_LAST_T(s2, s1, s0, s3);
+  const uint32_t o3 = GAES_LAST_T(s3, s2, s1, s0);
+#undef GAES_LAST_T
+  s0 = o0; s1 = o1; s2 = o2; s3 = o3;
+}
+
 }  // namespace gaes

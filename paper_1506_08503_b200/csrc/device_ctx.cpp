@@ -124,7 +124,7 @@ int get_ctx(int dev, DevCtx** out) {
   GAES_CK(cudaMalloc(&c->d_inv, 256));
   GAES_CK(cudaMemcpy(c->d_sbox, d_box, 256, cudaMemcpyDeviceToDevice));
   GAES_CK(cudaMemcpy(c->d_inv, d_box + 256, 256, cudaMemcpyDeviceToDevice));
-  if (env_int("GAES_TEXS", 1) != 0) {
+  if (tune_int("TEXS", 1) != 0) {
     c->tex_s_enc = make_byte_texture(c->d_sbox);
     c->tex_s_dec = make_byte_texture(c->d_inv);
   }
@@ -258,7 +258,7 @@ unsigned long long buffer_id(const void* p) {
 // that read it (its per-stream events); entries lent out right now are never
 // evicted.
 TexLease tex_for(DevCtx* c, const void* ptr, size_t bytes, cudaStream_t stream) {
-  static const bool enabled = env_int("GAES_TEXIN", 1) != 0;
+  static const bool enabled = tune_int("TEXIN", 1) != 0;
   if (!enabled || !ptr || bytes < 16) return {};
   // A launch captured into a CUDA graph may be replayed long after this
   // cache evicted (destroyed) the texture object; captured launches use LDG.
@@ -425,7 +425,7 @@ host::HostPool* device_pool(DevCtx* c) {
 
 int ilp_default() {
   // ILP 1 measured ~1% faster than 2 at configs 2 and 3 (finer tail, 40 regs)
-  static int ilp = std::max(1, std::min(2, env_int("GAES_ILP", 1)));
+  static int ilp = std::max(1, std::min(2, tune_int("ILP", 1)));
   return ilp;
 }
 
@@ -437,9 +437,18 @@ cudaError_t launch_enc_folded(DevCtx* c, const void* in, void* out, uint64_t n, 
     note_kernel("k_bs_blocks");
     return launch_bs_blocks(in, out, n, bk, c->sms, s);
   }
-  const cudaTextureObject_t tsb = sbox_tex(c, compact);
-  note_kernel(tsb ? "k_blocks_enc_folded+texsbox" : "k_blocks_enc_folded");
-  return launch_blocks(false, kIvFolded, ilp, in, out, n, compact, k, nullptr, 1, c->sms, s, tin, 0, tsb);
+  return launch_folded(c, false, in, out, n, compact, k, s, tin);
+}
+
+cudaError_t launch_folded(DevCtx* c, bool dec, const void* in, void* out, uint64_t n, const uint32_t* compact,
+                          const RoundKeys& k, cudaStream_t s, cudaTextureObject_t tin) {
+  const cudaTextureObject_t tsb = sbox_tex(c, compact);  // nonzero only for the GF layer's tables
+  if (tsb && n <= small_blocks_max(c->sms) && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+    note_kernel(dec ? "k_blocks_small_dec" : "k_blocks_small_enc");
+    return launch_blocks_small(dec, in, out, n, dec ? c->std_td : c->std_te, k, c->sms, s, tsb);
+  }
+  note_kernel(dec ? "k_blocks_dec_folded" : (tsb ? "k_blocks_enc_folded+texsbox" : "k_blocks_enc_folded"));
+  return launch_blocks(dec, kIvFolded, ilp_default(), in, out, n, compact, k, nullptr, 1, c->sms, s, tin, 0, tsb);
 }
 
 }  // namespace rt

@@ -29,6 +29,7 @@ struct Slot {
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
   uint8_t *h_in = nullptr, *h_out = nullptr, *h_iv = nullptr;  // pinned staging
+  uint8_t *dv_in = nullptr, *dv_out = nullptr, *dv_iv = nullptr;  // their device views (small zero-copy jobs)
   uint8_t *d_in = nullptr, *d_out = nullptr, *d_iv = nullptr;
   size_t cap = 0, iv_cap = 0;
   // pending D2H copy-out (pageable destination)
@@ -284,6 +285,11 @@ cudaTextureObject_t sbox_tex(const DevCtx* c, const uint32_t* compact);
 // (profiles/): T-table unless gaes_set_variant(2) selects the bitsliced kernel.
 cudaError_t launch_enc_folded(DevCtx* c, const void* in, void* out, uint64_t n, const uint32_t* compact,
                               const RoundKeys& k, int ilp, cudaStream_t s, cudaTextureObject_t tin);
+
+// M = 16 with the IV folded into the key (either direction): the small-batch
+// kernel for standard tables and n <= small_blocks_max, else k_blocks.
+cudaError_t launch_folded(DevCtx* c, bool dec, const void* in, void* out, uint64_t n, const uint32_t* compact,
+                          const RoundKeys& k, cudaStream_t s, cudaTextureObject_t tin);
 
 // Runs fn(offset, count) over [0, n) in texture-sized segments.
 template <typename F>

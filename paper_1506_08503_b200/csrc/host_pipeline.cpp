@@ -46,13 +46,30 @@ const uint8_t* host_dev_view(const void* p) {
 
 // Jobs up to this size on pinned caller buffers run as one zero-copy launch.
 size_t zero_copy_bytes() {
-  static size_t b = (size_t)std::max(0, env_int("GAES_ZEROCOPY_MB", 64)) << 20;
+  static size_t b = (size_t)std::max(0, tune_int("ZEROCOPY_MB", 64)) << 20;
+  return b;
+}
+
+// Pageable jobs up to this size run as one kernel on the pinned staging
+// buffers (see run_job).
+size_t small_zero_copy_bytes() {
+  static size_t b = (size_t)std::max(0, tune_int("SMALL_ZEROCOPY_KB", 1024)) << 10;
   return b;
 }
 
 size_t chunk_bytes() {
-  static size_t b = (size_t)std::max(1, env_int("GAES_CHUNK_MB", 32)) << 20;
+  static size_t b = (size_t)std::max(1, tune_int("CHUNK_MB", 32)) << 20;
   return b;
+}
+
+// Device address of pinned staging memory (nullptr if it has none).
+static uint8_t* dev_view(uint8_t* h) {
+  void* d = nullptr;
+  if (!h || cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return static_cast<uint8_t*>(d);
 }
 
 int ensure_slot(Slot& s, size_t bytes, size_t iv_bytes, bool staged_in, bool staged_out) {
@@ -61,21 +78,28 @@ int ensure_slot(Slot& s, size_t bytes, size_t iv_bytes, bool staged_in, bool sta
     if (s.d_out) cudaFree(s.d_out);
     if (s.h_in) cudaFreeHost(s.h_in);
     if (s.h_out) cudaFreeHost(s.h_out);
-    s.d_in = s.d_out = s.h_in = s.h_out = nullptr;
+    s.d_in = s.d_out = s.h_in = s.h_out = s.dv_in = s.dv_out = nullptr;
     s.cap = 0;
     GAES_CK(cudaMalloc(&s.d_in, bytes));
     GAES_CK(cudaMalloc(&s.d_out, bytes));
     s.cap = bytes;
   }
-  if (staged_in && !s.h_in) GAES_CK(cudaMallocHost(&s.h_in, s.cap));
-  if (staged_out && !s.h_out) GAES_CK(cudaMallocHost(&s.h_out, s.cap));
+  if (staged_in && !s.h_in) {
+    GAES_CK(cudaMallocHost(&s.h_in, s.cap));
+    s.dv_in = dev_view(s.h_in);
+  }
+  if (staged_out && !s.h_out) {
+    GAES_CK(cudaMallocHost(&s.h_out, s.cap));
+    s.dv_out = dev_view(s.h_out);
+  }
   if (iv_bytes && s.iv_cap < iv_bytes) {
     if (s.d_iv) cudaFree(s.d_iv);
     if (s.h_iv) cudaFreeHost(s.h_iv);
-    s.d_iv = s.h_iv = nullptr;
+    s.d_iv = s.h_iv = s.dv_iv = nullptr;
     s.iv_cap = 0;
     GAES_CK(cudaMalloc(&s.d_iv, iv_bytes));
     GAES_CK(cudaMallocHost(&s.h_iv, iv_bytes));
+    s.dv_iv = dev_view(s.h_iv);
     s.iv_cap = iv_bytes;
   }
   return GAES_OK;
@@ -103,9 +127,7 @@ int launch_chunk(DevCtx* c, Lane* lane, const Job& j, cudaStream_t stream, const
   switch (j.mode) {
     case Mode::kFolded:
       if (j.dec) {
-        GAES_CK(launch_blocks(true, kIvFolded, ilp_default(), in, out, nblk, compact, j.rk, nullptr, 1,
-                              c->sms, stream, tin, 0, tsb));
-        note_kernel("k_blocks_dec_folded");
+        GAES_CK(launch_folded(c, true, in, out, nblk, compact, j.rk, stream, tin));
       } else if (j.standard || g_variant.load() < 2) {
         GAES_CK(launch_enc_folded(c, in, out, nblk, compact, j.rk, ilp_default(), stream,
                                   tin));
@@ -175,7 +197,7 @@ bool stage_and_check_iv(uint8_t* dst, const uint8_t* src, size_t m, const uint8_
 // reused call after call; lanes 1.. only for concurrent callers); if all
 // are busy, waits on one chosen by thread.
 std::unique_lock<std::mutex> lock_lane(DevCtx* c, Lane** out) {
-  static const int lanes = std::max(1, std::min(kLanes, env_int("GAES_LANES", kLanes)));
+  static const int lanes = std::max(1, std::min(kLanes, tune_int("LANES", kLanes)));
   for (int k = 0; k < lanes; k++) {
     std::unique_lock<std::mutex> lk(c->lanes[k].mu, std::try_to_lock);
     if (lk.owns_lock()) {
@@ -337,13 +359,47 @@ int run_job(DevCtx* c, const Job& j) {
       return GAES_OK;
     }
   }
+  // Small jobs on pageable caller buffers: stage into the lane's pinned
+  // buffer and let ONE kernel read it and write the pinned output staging
+  // over PCIe, instead of an H2D copy, a kernel and a D2H copy -- below
+  // ~1 MiB the two DMA round trips' fixed latency is most of the call.
+  // (Byte-level generic tables excluded, as for caller zero-copy.)
+  if (!in_pinned && !out_pinned && j.mode != Mode::kGeneric && total <= small_zero_copy_bytes()) {
+    Slot& s = lane->slots[0];
+    int rc = ensure_slot(s, std::max(total, (size_t)1 << 20), need_iv ? std::max(j.n * 16, (size_t)1 << 16) : 0,
+                         true, true);
+    if (rc) return rc;
+    if (s.dv_in && s.dv_out && (!need_iv || s.dv_iv)) {
+      bool shared = false;
+      if (j.auto_iv)
+        shared = stage_and_check_iv(s.h_in, j.data, j.m, j.ivs, j.n, j.iv0);
+      else
+        par_memcpy(s.h_in, j.data, total);
+      Job view;
+      const Job* jc = &j;
+      if (shared) {
+        view = j;
+        view.mode = j.mode_shared;
+        view.rk = j.rk_shared;
+        view.ivs = nullptr;
+        jc = &view;
+      }
+      if (jc->ivs) std::memcpy(s.h_iv, j.ivs, j.n * 16);
+      rc = launch_chunk(c, lane, *jc, s.stream, s.dv_in, s.dv_out, s.dv_iv, 0, j.n, compact, 0);
+      if (rc) return rc;
+      GAES_CK(cudaStreamSynchronize(s.stream));
+      par_memcpy(j.out, s.h_out, total);
+      drain.armed = false;
+      return GAES_OK;
+    }
+  }
   // Chunk schedule: ramp up from base/8 so the first H2D is short (nothing
   // overlaps it), run at `base`, ramp down at the end so the last D2H is
   // short too.  All chunks are whole rows.
   // Pageable buffers are staged by host copies: smaller chunks let the copy
   // of chunk c+1 overlap the DMA of chunk c.
   // pageable callers: 16 MiB (17.0 vs 16.3 / 15.2 GB/s with 8 / 4 MiB, 16 threads)
-  static const size_t pageable_chunk = (size_t)std::max(1, env_int("GAES_PAGEABLE_CHUNK_MB", 16)) << 20;
+  static const size_t pageable_chunk = (size_t)std::max(1, tune_int("PAGEABLE_CHUNK_MB", 16)) << 20;
   const size_t base_bytes = (in_pinned && out_pinned) ? chunk_bytes() : std::min<size_t>(chunk_bytes(), pageable_chunk);
   const size_t base_rows = std::max<size_t>(1, base_bytes / j.m);
   // (splitting small staged jobs further was measured slower: per-chunk

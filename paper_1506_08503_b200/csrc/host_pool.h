@@ -20,6 +20,8 @@
 #include <immintrin.h>
 #endif
 
+#include "runtime.h"
+
 namespace gaes {
 namespace host {
 
@@ -273,10 +275,7 @@ __attribute__((target("avx2"))) inline void nt_copy_avx2(uint8_t* dst, const uin
 
 inline bool nt_copies() {
 #if defined(__x86_64__)
-  static const bool on = [] {
-    const char* e = std::getenv("GAES_NT");
-    return !(e && e[0] == '0') && __builtin_cpu_supports("avx2");
-  }();
+  static const bool on = rt::tune_int("NT", 1) != 0 && __builtin_cpu_supports("avx2");
   return on;
 #else
   return false;
@@ -295,10 +294,7 @@ inline void stage_copy(void* dst, const void* src, size_t bytes) {
 }
 
 inline void par_memcpy(void* dst, const void* src, size_t bytes) {
-  static const size_t grain = [] {
-    const char* e = std::getenv("GAES_MEMCPY_GRAIN_KB");
-    return (size_t)std::max(16, (e && *e) ? std::atoi(e) : 128) << 10;
-  }();
+  static const size_t grain = (size_t)std::max(16, rt::tune_int("MEMCPY_GRAIN_KB", 128)) << 10;
   parallel_ranges(bytes, grain, [&](size_t lo, size_t hi) {
     stage_copy((uint8_t*)dst + lo, (const uint8_t*)src + lo, hi - lo);
   });

@@ -30,6 +30,7 @@
 #include "aes_ttable.cuh"
 #include "gf.cuh"
 #include "kernels.h"
+#include "runtime.h"
 #include "tma.cuh"
 
 namespace gaes {
@@ -221,6 +222,52 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
     }
 #pragma unroll
     for (int k = 0; k < ILP; k++) cur[k] = nxt[k];
+    b = nb;
+  }
+}
+
+// Small batches: see launch_blocks_small (kernels.h) and encrypt_rounds_rot
+// (aes_ttable.cuh).  One block per thread; the CTA size is chosen so that a
+// batch spreads evenly over the SMs.  The table fill reads only the kernel
+// parameters, so it runs before griddepcontrol.wait -- while the previous
+// launch on the stream is still computing, on the same SM (64 KiB and at
+// most 512 threads per CTA leave room for it).
+template <bool DEC>
+__global__ void __launch_bounds__(kSmallThreads, 3)
+    k_blocks_small(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks,
+                   const __grid_constant__ SmallTables st, const __grid_constant__ RoundKeys rk,
+                   cudaTextureObject_t tsb) {
+  extern __shared__ __align__(1024) char smem[];
+  asm volatile("griddepcontrol.launch_dependents;");
+  // region 0: entry x at 256 x, words 0-31 = T0[x] (32 lane copies), 32-63 = T1[x] = rotl8(T0[x])
+  for (int q = threadIdx.x; q < 2 * 256 * 8; q += blockDim.x) {
+    const int quad = q & 7, x = (q >> 3) & 255, tbl = q >> 11;
+    const uint32_t t = st.t0[x];
+    const uint32_t v = tbl ? __funnelshift_l(t, t, 8) : t;
+    *reinterpret_cast<uint4*>(smem + x * 256 + tbl * 128 + quad * 16) = make_uint4(v, v, v, v);
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const uint32_t lb = (threadIdx.x & 31) * 4;
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n_blocks) return;
+  uint4 cur = ld_stream(in + b);
+  while (b < n_blocks) {
+    const uint64_t nb = b + T;
+    uint4 nxt = cur;
+    if (nb < n_blocks) nxt = ld_stream(in + nb);
+    uint32_t s0 = cur.x, s1 = cur.y, s2 = cur.z, s3 = cur.w;
+    if (!DEC) {
+      s0 ^= rk.w[0]; s1 ^= rk.w[1]; s2 ^= rk.w[2]; s3 ^= rk.w[3];
+      encrypt_rounds_rot(smem, lb, s0, s1, s2, s3, rk, tsb);
+    } else {
+      s0 ^= rk.w[40]; s1 ^= rk.w[41]; s2 ^= rk.w[42]; s3 ^= rk.w[43];
+      decrypt_rounds_rot(smem, lb, s0, s1, s2, s3, rk, tsb);
+      s0 ^= rk.w[0]; s1 ^= rk.w[1]; s2 ^= rk.w[2]; s3 ^= rk.w[3];
+    }
+    st_stream(out + b, make_uint4(s0, s1, s2, s3));
+    cur = nxt;
     b = nb;
   }
 }
@@ -685,10 +732,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  static const bool pdl = [] {
-    const char* e = std::getenv("GAES_PDL");
-    return !(e && e[0] == '0');
-  }();
+  static const bool pdl = rt::tune_int("PDL", 1) != 0;
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
@@ -730,10 +774,7 @@ static cudaError_t launch_blocks_t(const void* in, void* out, uint64_t n, const 
   if (e != cudaSuccess) return e;
   // every SM that gets at least one warp's 32 blocks (see k_blocks' map)
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(sms, (n + 31) / 32));
-  static const int early_mode = [] {
-    const char* e = std::getenv("GAES_EARLY");
-    return (e && *e) ? std::atoi(e) : 2;  // 0 never, 1 always, 2 single-pass batches
-  }();
+  static const int early_mode = rt::tune_int("EARLY", 2);  // 0 never, 1 always, 2 single-pass batches
   const int early = early_mode == 1 || (early_mode == 2 && n <= (uint64_t)grid * kBlockThreads * ILP);
   return launch_pdl(kern, grid, kBlockThreads, kSmemBytes, s, (const uint4*)in, (uint4*)out, n, compact, rk,
                     (const uint4*)ivs, bpr, tin, tiv, early, tsb);
@@ -773,6 +814,27 @@ cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* o
   GAES_CASE(2, false, kIvChain) GAES_CASE(2, true, kIvChain)
 #undef GAES_CASE
   return cudaErrorInvalidValue;
+}
+
+uint64_t small_blocks_max(int sms) {
+  static const int per_sm = std::max(0, rt::tune_int("SMALL_BLOCKS_PER_SM", 3 * kSmallThreads));
+  return (uint64_t)sms * per_sm;
+}
+
+cudaError_t launch_blocks_small(bool dec, const void* in, void* out, uint64_t n, const uint32_t* t0,
+                                const RoundKeys& rk, int sms, cudaStream_t s, cudaTextureObject_t tsb) {
+  if (n == 0) return cudaSuccess;
+  auto kern = dec ? k_blocks_small<true> : k_blocks_small<false>;
+  cudaError_t e = set_smem(kern, kSmallSmemBytes);
+  if (e != cudaSuccess) return e;
+  SmallTables st;
+  for (int i = 0; i < 256; i++) st.t0[i] = t0[i];
+  // threads per CTA: the batch spread evenly over the SMs (whole warps,
+  // 128..512), up to 3 CTAs per SM beyond that
+  uint64_t per_sm = (n + sms - 1) / sms;
+  int threads = (int)std::min<uint64_t>(kSmallThreads, std::max<uint64_t>(128, (per_sm + 31) & ~(uint64_t)31));
+  const uint64_t ctas = std::min<uint64_t>((uint64_t)3 * sms, (n + threads - 1) / threads);
+  return launch_pdl(kern, (int)ctas, threads, kSmallSmemBytes, s, (const uint4*)in, (uint4*)out, n, st, rk, tsb);
 }
 
 // Row-CBC geometry: a thread owns whole rows, so the launch is sized in
@@ -827,15 +889,12 @@ static bool rows_tensor_map(CUtensorMap* map, const void* base, uint64_t n_rows,
 }
 
 // TMA row kernel: texture S-box, even blocks per row >= 8, 16-byte aligned
-// grids, coordinates inside int32; GAES_ROWS_TMA=0 disables it.
+// grids, coordinates inside int32; GAES_TUNE=ROWS_TMA=0 disables it.
 static cudaError_t launch_cbc_enc_rows_tma(const void* in, void* out, uint64_t n_rows, uint64_t bpr,
                                            const uint32_t* compact, const RoundKeys& rk, const void* ivs, int sms,
                                            cudaStream_t s, cudaTextureObject_t tsb, bool* launched) {
   *launched = false;
-  static const bool enabled = [] {
-    const char* e = std::getenv("GAES_ROWS_TMA");
-    return !(e && *e && std::atoi(e) == 0);
-  }();
+  static const bool enabled = rt::tune_int("ROWS_TMA", 1) != 0;
   const uint64_t m = bpr * 16;
   if (!enabled || !tsb || bpr < 8 || (bpr & 1) || n_rows < 32 || n_rows > 0x7FFFFFF0ull || m > 0x7FFFFFF0ull ||
       ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15))
@@ -845,10 +904,7 @@ static cudaError_t launch_cbc_enc_rows_tma(const void* in, void* out, uint64_t n
   // the LDG/STG kernel is as fast or faster (scripts/exp/rows_threshold.sh,
   // 2^24 blocks: 13.8 groups/SM -- 2^16 rows of 256 blocks -- 709 vs 671 GB/s
   // TMA vs LDG; 6.9 groups/SM 540 vs 543; 3.5 groups/SM 342 vs 361).
-  static const uint64_t min_groups_per_sm = [] {
-    const char* e = std::getenv("GAES_ROWS_TMA_MIN_GROUPS");  // per SM; tests set 0
-    return (uint64_t)((e && *e) ? std::max(0, std::atoi(e)) : 8);
-  }();
+  static const uint64_t min_groups_per_sm = (uint64_t)std::max(0, rt::tune_int("ROWS_TMA_MIN_GROUPS", 8));  // per SM; tests set 0
   const uint64_t groups = (n_rows + 31) / 32;
   if (groups < (uint64_t)sms * min_groups_per_sm) return cudaSuccess;
   CUtensorMap tmi, tmo;

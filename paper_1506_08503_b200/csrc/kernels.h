@@ -10,6 +10,8 @@ namespace gaes {
 
 static constexpr int kBlockThreads = 1024;     // k_blocks / k_cbc_enc_rows: 1 CTA per SM
 static constexpr int kManyKeyThreads = 768;    // k_many_key: 44 round-key registers per thread (<= 85 regs)
+static constexpr int kSmallThreads = 512;      // k_blocks_small: up to 3 CTAs per SM (PDL co-residence)
+static constexpr int kSmallSmemBytes = 65536;  // region 0 (T0 | T1)
 static constexpr int kBsThreads = 128;         // k_bs_blocks: ~170 registers per thread
 static constexpr int kBsCtasPerSm = 3;
 static constexpr int kIvFolded = 0;
@@ -26,6 +28,13 @@ cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* o
                           const uint32_t* compact, const RoundKeys& rk, const void* ivs, uint64_t bpr, int sms,
                           cudaStream_t s, cudaTextureObject_t tin = 0, cudaTextureObject_t tiv = 0,
                           cudaTextureObject_t tsb = 0);
+// Small batches (n <= small_blocks_max(sms)), shared IV folded into the key,
+// standard tables (t0 = Te0 / Td0 of the GF layer, tsb its S-box texture):
+// k_blocks_small -- 64 KiB of tables filled from the kernel parameters, up
+// to 3 CTAs per SM so the next launch fills while this one computes.
+uint64_t small_blocks_max(int sms);
+cudaError_t launch_blocks_small(bool dec, const void* in, void* out, uint64_t n_blocks, const uint32_t* t0,
+                                const RoundKeys& rk, int sms, cudaStream_t s, cudaTextureObject_t tsb);
 // Row CBC encrypt: the TMA-staged kernel when it applies (texture S-box,
 // >= 8 even blocks per row, enough rows), else the LDG/STG kernel.
 bool last_rows_launch_used_tma();  // on this thread

@@ -31,5 +31,21 @@ int env_int(const char* name, int dflt) {
   return std::atoi(v);
 }
 
+int tune_int(const char* key, int dflt) {
+  const char* v = std::getenv("GAES_TUNE");
+  if (!v || !*v) return dflt;
+  const std::string all(v), k(key);
+  size_t pos = 0;
+  while (pos < all.size()) {
+    size_t end = all.find(',', pos);
+    if (end == std::string::npos) end = all.size();
+    const std::string item = all.substr(pos, end - pos);
+    const size_t eq = item.find('=');
+    if (eq != std::string::npos && item.substr(0, eq) == k) return std::atoi(item.c_str() + eq + 1);
+    pos = end + 1;
+  }
+  return dflt;
+}
+
 }  // namespace rt
 }  // namespace gaes

@@ -17,6 +17,12 @@ static constexpr int kOffS = 2 * kRegionBytes;
 //   t[0..3][x] = T0..T3, t[4][x] = S[x] (low byte).
 static constexpr int kCompactWords = 5 * 256;
 
+// T0 (encrypt Te0 or decrypt Td0) for the small-batch kernel's fill, passed
+// as a kernel parameter (constant bank).
+struct SmallTables {
+  uint32_t t0[256];
+};
+
 struct RoundKeys {
   // encrypt: w[4r+c] = LE word of rk[r][4c..4c+3]   (r = 0..10)
   // decrypt: w[0..3] = rk0, w[4r+c] = InvMix(rk_r) for r = 1..9, w[40..43] = rk10
