@@ -152,7 +152,8 @@ def pieces(cfg: int, blocks: int | None = None) -> list:
 
 def l2_policy(cfg: int, world: int) -> str:
     lo, hi = rank_range(cfg, 0, world)
-    return "L2 flushed between steps" if (hi - lo) * 32 < (256 << 20) else "inputs larger than L2 (no flush)"
+    return ("ring of K cold copies of the batch (one L2 flush before the region), K steps as one CUDA graph"
+            if (hi - lo) * 32 < (256 << 20) else "inputs larger than L2 (no flush)")
 
 
 def workload_params(cfg: int, blocks: int | None = None) -> dict:
@@ -911,16 +912,44 @@ def main(argv=None):
         def step():
             cipher.encrypt(p, out=out)
 
-    flush = None
-    if n * 32 < 256 << 20:  # working set below 2x L2: flush L2 between timed steps
-        flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    small = n * 32 < 256 << 20  # working set below 2x L2
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if small else None
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
 
-    # ---- timed region: CUDA events on the launching stream (per step when L2 is
-    # flushed between steps, else one pair around K back-to-back steps)
+    def capture(fn, k):
+        """fn(i) for i < k as one CUDA graph (k launches); returns (graph, launches)."""
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            fn(0)  # first-use work (smem opt-in, textures) stays outside the capture
+        torch.cuda.current_stream().wait_stream(side)
+        l0 = _lib.launch_count()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(k):
+                fn(i)
+        return g, _lib.launch_count() - l0
+
+    graph = None
+    if small:
+        # Small batches (config 1): the K timed steps encrypt K distinct
+        # copies of the batch -- a ring of inputs and outputs that one L2
+        # flush before the region makes cold, so every step reads its input
+        # from HBM ("inputs larger than L2") -- submitted as one CUDA graph of
+        # K launches: the B200 way to issue a stream of small batches without
+        # the host's per-launch enqueue cost (~4 us) on every step.
+        ring_in = p.unsqueeze(0).repeat(args.steps, 1, 1)
+        ring_out = torch.empty_like(ring_in)
+        graph, graph_launches = capture(lambda i: cipher.encrypt(ring_in[i], out=ring_out[i]), args.steps)
+        graph.replay()
+        torch.cuda.synchronize()
+
+    # ---- timed region: one pair of CUDA events on the launching stream around
+    # K back-to-back steps (inputs larger than L2), or around the graph of K
+    # steps on the cold ring (small batches)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(_smi_index(gpu)) as clk:
@@ -937,43 +966,59 @@ def main(argv=None):
         torch.cuda.synchronize()
         mark = clk.mark()
         t_timed = time.perf_counter()
-        # one untimed step keeps the GPU busy while the host enqueues the
-        # first timed step, so step 0's start event does not absorb the
-        # Python launch latency of an empty queue; the events below bracket
-        # exactly K steps.
-        step()
         launches0 = _lib.launch_count()
-        if flush is not None:
-            # small working set: flush L2 between steps, each step bracketed
-            # by its own events (the flush is outside them)
-            for i in range(args.steps):
-                flush.fill_(i & 0xFF)
-                starts[i].record(stream)
-                step()
-                ends[i].record(stream)
+        if graph is not None:
+            flush.fill_(1)  # evicts the whole ring (and keeps the GPU busy while the host enqueues)
+            starts[0].record(stream)
+            graph.replay()
+            ends[0].record(stream)
+            torch.cuda.synchronize()
+            launches = graph_launches
         else:
-            # inputs larger than L2: the K steps run back to back between one
-            # pair of events (no event between launches, so a launch can
-            # start its CTAs while the previous one drains)
+            # one untimed step keeps the GPU busy while the host enqueues the
+            # first timed step, so the start event does not absorb the Python
+            # launch latency of an empty queue; the events bracket exactly K
+            # steps, no event between launches (a launch starts its CTAs
+            # while the previous one drains)
+            step()
+            launches0 = _lib.launch_count()
             starts[0].record(stream)
             for i in range(args.steps):
                 step()
             ends[0].record(stream)
-        torch.cuda.synchronize()
-        launches = _lib.launch_count() - launches0
+            torch.cuda.synchronize()
+            launches = _lib.launch_count() - launches0
         # ---- wall span: host barrier -> the last rank's
         # completion of K more steps, on the host's monotonic clock (shared
         # by the ranks of one node); events do not see skew between ranks.
         if launched:
             dist.barrier()
         t_b = time.perf_counter()
-        for i in range(args.steps):
-            if flush is not None:
-                flush.fill_(i & 0xFF)
-            step()
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(args.steps):
+                step()
         torch.cuda.synchronize()
         t_e = time.perf_counter()
         span_s = max_over_ranks(t_e, reduce_dev) + max_over_ranks(-t_b, reduce_dev)
+        # small batches, the other way round: each step its own stream launch
+        # after an L2 flush, bracketed by its own events (reported beside the
+        # value: includes the 4-6 us of stream-launch + event overhead that an
+        # empty kernel shows the same way, profiles/r2/small_batches.md)
+        stream_steps = None
+        if small:
+            for i in range(args.steps):
+                flush.fill_(i & 0xFF)
+                starts[i].record(stream)
+                step()
+                ends[i].record(stream)
+            torch.cuda.synchronize()
+            sms_ = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+            stream_steps = {"ms_per_step": round(sum(sms_) / len(sms_), 5),
+                            "value": round(n * BYTES_PER_BLOCK / (sum(sms_) / len(sms_) / 1e3) / 1e9, 2),
+                            "unit": "GB/s per GPU",
+                            "note": "per step: L2 flush, event, one stream launch, event"}
         while time.perf_counter() - t_timed < 0.5:
             step()
             torch.cuda.synchronize()
@@ -982,10 +1027,10 @@ def main(argv=None):
     clocks["window"] = "timed region + same-kernel soak to >= 0.5 s"
     clocks["throttled"] = any(r in clocks["reasons"] for r in
                               ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"))
-    if flush is not None:
-        ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    else:
-        ms = [starts[0].elapsed_time(ends[0]) / args.steps] * args.steps
+    ms = [starts[0].elapsed_time(ends[0]) / args.steps] * args.steps
+    if graph is not None:
+        assert torch.equal(ring_out[-1], ring_out[0])
+        out = ring_out[0]
     ms_local = sum(ms) / len(ms)
     ms_step = max_over_ranks(ms_local, reduce_dev)
     job_blocks = n * world if weak else total_blocks(cfg, world)
@@ -993,7 +1038,7 @@ def main(argv=None):
     wall_span = {"ms_per_step": round(span_s * 1e3 / args.steps, 4),
                  "value": round(job_blocks * BYTES_PER_BLOCK * args.steps / span_s / 1e9, 2), "unit": "GB/s",
                  "note": ("host barrier -> last rank's completion of K steps (host monotonic clock, all ranks); "
-                          + ("includes the L2 flush between steps" if flush is not None else "back-to-back steps"))}
+                          + ("one graph replay of the K-step ring" if graph is not None else "back-to-back steps"))}
 
     # ---- verification (outside the timed region).  The GPU arm does not
     # touch the oracle: configs 1/2 use the reference recipe, so the whole
@@ -1032,7 +1077,7 @@ def main(argv=None):
     verified &= bool(torch.equal(back, p))
     check["round_trip"] = bool(torch.equal(back, p))
 
-    # decrypt throughput (reported, not the metric): same event discipline
+    # decrypt throughput (reported, not the metric): same discipline
     def dstep():
         if cfg == 5:
             device.many_key_decrypt(out, rk_dec, d_ivs, out=back)
@@ -1042,19 +1087,20 @@ def main(argv=None):
         dstep()
     torch.cuda.synchronize()
     dreps = max(3, min(args.steps, 10))
-    if flush is not None:
-        dms = []
-        for _ in range(dreps):
-            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            flush.fill_(7)
-            ev0.record(stream)
-            dstep()
-            ev1.record(stream)
-            dms.append((ev0, ev1))
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if small:
+        ring_back = torch.empty_like(ring_out)
+        dgraph, _ = capture(lambda i: cipher.decrypt(ring_out[i], out=ring_back[i]), args.steps)
+        dgraph.replay()
+        flush.fill_(7)
+        ev0.record(stream)
+        dgraph.replay()
+        ev1.record(stream)
         torch.cuda.synchronize()
-        dec_ms = sum(a.elapsed_time(b) for a, b in dms) / len(dms)
+        dec_ms = ev0.elapsed_time(ev1) / args.steps
+        assert torch.equal(ring_back[-1], p)
+        del ring_back
     else:
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         dstep()
         ev0.record(stream)
         for _ in range(dreps):
@@ -1097,7 +1143,8 @@ def main(argv=None):
             "config": config_dict(cfg, world),
             "dist": {"backend": backend, "ranks": world, "gpus_visible": ndev,
                      "host_cpus": (f"{len(numa_cpus)} CPUs local to the GPU" if numa_cpus else "all")},
-            "gpu_launches": launches, "wall_span": wall_span, "roofline": roofline, "e2e": e2e,
+            "gpu_launches": launches, "wall_span": wall_span, "stream_launch_steps": stream_steps,
+            "roofline": roofline, "e2e": e2e,
             "e2e_dropin": dropin, "cpu_baseline": cpu, "cpu_openssl": openssl, "clocks": clocks,
             "decrypt_gbs_per_gpu": round(dec_gbs, 2), "verified": bool(verified_all), "verification": check,
             "digests": sorted((x for d in all_digests for x in d["digests"]), key=lambda x: (x["blocks"], x["rank"])),

@@ -11,7 +11,7 @@ python bench.py --config 3 --steps 10 --warmup 3 --no-cpu-baseline > $O/bench_cf
 python scripts/profile_kernels.py encrypt 24 > $O/plain_tex.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:k_blocks -s 3 -c 1 \
       -o $O/ttable_src python scripts/profile_kernels.py encrypt 24 > $O/ncu_tex.log 2>&1
-GAES_TEXS=0 GAES_TEXIN=0 python scripts/profile_kernels.py encrypt 24 > $O/plain_notex.log 2>&1 && \
-  GAES_TEXS=0 GAES_TEXIN=0 ncu --set full --clock-control none --import-source on -k regex:k_blocks -s 3 -c 1 \
+GAES_TUNE=TEXS=0,TEXIN=0 python scripts/profile_kernels.py encrypt 24 > $O/plain_notex.log 2>&1 && \
+  GAES_TUNE=TEXS=0,TEXIN=0 ncu --set full --clock-control none --import-source on -k regex:k_blocks -s 3 -c 1 \
       -o $O/ttable_notex_src python scripts/profile_kernels.py encrypt 24 > $O/ncu_notex.log 2>&1
 ls -la $O

@@ -791,7 +791,7 @@ def _pinned(shape, rng=None):
 
 @pytest.mark.parametrize("n,m", [(1, 16), (4097, 16), (4096, 16), (3001, 64), (1 << 20, 16)])
 def test_pinned_zero_copy_every_mode(oracle, n, m):
-    """Pinned host buffers up to GAES_ZEROCOPY_MB run as one zero-copy launch
+    """Pinned host buffers up to 64 MiB (GAES_TUNE ZEROCOPY_MB) run as one zero-copy launch
     (the kernel reads and writes host memory over PCIe); every host entry
     point must match the oracle there, with pinned per-row IVs too, and
     in-place pinned calls (which take the staged pipeline) as well."""
@@ -1004,7 +1004,7 @@ def test_cuda_graph_capture_and_replay(oracle):
 
 
 def test_shared_memory_sbox_path_without_textures():
-    """GAES_TEXS=0 / GAES_TEXIN=0 (the paths used when textures are
+    """GAES_TUNE=TEXS=0,TEXIN=0 (the paths used when textures are
     unavailable): round 10 reads the replicated S table in shared memory and
     inputs come through LDG -- bit-exact against the oracle for every kernel."""
     import os
@@ -1036,7 +1036,7 @@ assert np.array_equal(c[:5000], oracle.encrypt(keys[0].tobytes(), np.zeros((5000
 assert np.array_equal(backend_cuda.many_key_decrypt(c, keys), p)
 print("ok")
 '''
-    env = dict(os.environ, GAES_TEXS="0", GAES_TEXIN="0")
+    env = dict(os.environ, GAES_TUNE="TEXS=0,TEXIN=0")
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
@@ -1058,7 +1058,7 @@ def test_row_cbc_tma_path_matches_oracle(oracle, blocks):
     x = torch.from_numpy(p).cuda()
     want = oracle.encrypt(key, ivs, p, threads=8)
     c = device.cbc_encrypt(x, rk, torch.from_numpy(ivs).cuda())
-    if _lib.lib().gaes_uses_sbox_texture(0) == 1 and os.environ.get("GAES_ROWS_TMA", "1") != "0":
+    if _lib.lib().gaes_uses_sbox_texture(0) == 1 and "ROWS_TMA=0" not in os.environ.get("GAES_TUNE", ""):
         assert _lib.last_kernel() == "k_cbc_enc_rows_tma"
     assert np.array_equal(c.cpu().numpy(), want)
     assert torch.equal(device.cbc_decrypt(c, rk, torch.from_numpy(ivs).cuda()), x)
@@ -1073,7 +1073,7 @@ def test_row_cbc_tma_path_matches_oracle(oracle, blocks):
 
 def test_row_cbc_tma_kernel_at_any_row_count():
     """The TMA row kernel itself (forced for every row count with
-    GAES_ROWS_TMA_MIN_GROUPS=0, normally only used from 8 row groups per
+    GAES_TUNE=ROWS_TMA_MIN_GROUPS=0, normally only used from 8 row groups per
     SM): 1..4 warps with rows, ragged groups, 8..64-block rows."""
     import subprocess
     import sys
@@ -1093,7 +1093,7 @@ for n, bpr in [(32, 8), (33, 64), (100, 16), (1500, 8), (4737, 10)]:
     assert np.array_equal(c.cpu().numpy(), oracle.encrypt(key, ivs, p, threads=4)), (n, bpr)
 print("ok")
 '''
-    env = dict(os.environ, GAES_ROWS_TMA_MIN_GROUPS="0")
+    env = dict(os.environ, GAES_TUNE="ROWS_TMA_MIN_GROUPS=0")
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True, text=True, timeout=300)
     if "k_cbc_enc_rows\n" in r.stderr or _lib.lib().gaes_uses_sbox_texture(0) != 1:
