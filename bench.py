@@ -988,6 +988,7 @@ def main(argv=None):
             ends[0].record(stream)
             torch.cuda.synchronize()
             launches = _lib.launch_count() - launches0
+        ms = [starts[0].elapsed_time(ends[0]) / args.steps] * args.steps
         # ---- wall span: host barrier -> the last rank's
         # completion of K more steps, on the host's monotonic clock (shared
         # by the ranks of one node); events do not see skew between ranks.
@@ -1008,13 +1009,15 @@ def main(argv=None):
         # empty kernel shows the same way, profiles/r2/small_batches.md)
         stream_steps = None
         if small:
+            s_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    for _ in range(args.steps)]
             for i in range(args.steps):
                 flush.fill_(i & 0xFF)
-                starts[i].record(stream)
+                s_ev[i][0].record(stream)
                 step()
-                ends[i].record(stream)
+                s_ev[i][1].record(stream)
             torch.cuda.synchronize()
-            sms_ = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+            sms_ = [a.elapsed_time(b) for a, b in s_ev]
             stream_steps = {"ms_per_step": round(sum(sms_) / len(sms_), 5),
                             "value": round(n * BYTES_PER_BLOCK / (sum(sms_) / len(sms_) / 1e3) / 1e9, 2),
                             "unit": "GB/s per GPU",
@@ -1027,7 +1030,6 @@ def main(argv=None):
     clocks["window"] = "timed region + same-kernel soak to >= 0.5 s"
     clocks["throttled"] = any(r in clocks["reasons"] for r in
                               ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"))
-    ms = [starts[0].elapsed_time(ends[0]) / args.steps] * args.steps
     if graph is not None:
         assert torch.equal(ring_out[-1], ring_out[0])
         out = ring_out[0]

@@ -47,6 +47,7 @@ def is_stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not is_stale():
+        build_pyfast()
         return LIB_PATH
     nvcc = _nvcc()
     objdir = os.path.join(PKG_DIR, "build")
@@ -62,7 +63,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB_PATH + ".tmp"
     subprocess.check_call([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lpthread"])
     os.replace(tmp, LIB_PATH)
+    build_pyfast(force=True)
     return LIB_PATH
+
+
+def build_pyfast(force: bool = False) -> str:
+    """csrc/pyfast.c -> _pyfast<EXT_SUFFIX>: the CPython fast path of the
+    drop-in calls (argument checks + C-ABI call without Python-level
+    pointer extraction), linked against libgaes_b200.so."""
+    import sysconfig
+    out = os.path.join(PKG_DIR, "_pyfast" + sysconfig.get_config_var("EXT_SUFFIX"))
+    src = os.path.join(CSRC, "pyfast.c")
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(src),
+                                                                          os.path.getmtime(LIB_PATH)):
+        return out
+    tmp = out + ".tmp"
+    subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-fvisibility=hidden", "-I", sysconfig.get_paths()["include"],
+                           "-I", os.path.join(REPO, "include"), src, "-o", tmp, "-L", PKG_DIR, "-l:libgaes_b200.so",
+                           "-Wl,-rpath,$ORIGIN"])
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

@@ -183,3 +183,38 @@ def test_debug_counters_without_a_gpu():
     c = _lib.debug_counters()
     assert set(c) == set(_lib.DEBUG_COUNTERS)
     assert all(v >= 0 for v in c.values())
+
+
+def test_pyfast_defers_every_irregular_argument_to_the_checked_path():
+    """csrc/pyfast.c only takes plain C-contiguous uint8 buffers of the
+    contract's shapes; anything else returns None so backend_cuda's Python
+    checks raise the reference's messages (no GPU needed: valid calls reach
+    the C ABI, which reports the missing device)."""
+    import numpy as np
+
+    from paper_1506_08503_b200 import _pyfast, backend_cuda
+    d = np.zeros((8, 32), np.uint8)
+    iv = np.zeros((8, 16), np.uint8)
+    rk = np.zeros((11, 16), np.uint8)
+    box, lut, perm = np.zeros(256, np.uint8), np.zeros((4, 4, 256), np.uint8), np.arange(16, dtype=np.uint8)
+    out = np.empty_like(d)
+    args = [d, iv, rk, box, lut, perm, out]
+    assert isinstance(_pyfast.cbc(False, *args), int)
+    bad = {0: [d.view(np.int8), d[:, :16], d.reshape(-1), d.astype(np.uint16)],
+           1: [iv[:4], np.zeros((8, 8), np.uint8)], 2: [rk[:10], rk.reshape(-1)], 3: [box[:255]],
+           4: [lut.reshape(16, 256)], 5: [perm + 16, perm[:8]],
+           6: [np.frombuffer(bytes(256), np.uint8).reshape(8, 32), out[:4], out[:, ::2]]}
+    for i, variants in bad.items():
+        for v in variants:
+            a = list(args)
+            a[i] = v
+            assert _pyfast.cbc(False, *a) is None, (i, getattr(v, "shape", None))
+    assert _pyfast.cbc(True, [[0] * 16], iv, rk, box, lut, perm, out) is None  # not a buffer
+    assert _pyfast.shared_iv(False, d, bytes(16), bytes(176), out) is not None
+    assert _pyfast.shared_iv(False, d, bytes(15), bytes(176), out) is None
+    assert _pyfast.shared_iv(False, d, np.zeros(2, np.int64), rk, out) is None
+    # the Python path behind it still raises the reference's messages
+    with pytest.raises(ValueError, match="Buffer dtype mismatch"):
+        backend_cuda.cbc_encrypt(d.view(np.int8), iv, rk, box, lut, perm, out)
+    with pytest.raises(ValueError, match="read-only"):
+        backend_cuda.cbc_encrypt(d, iv, rk, box, lut, perm, np.frombuffer(bytes(256), np.uint8).reshape(8, 32))

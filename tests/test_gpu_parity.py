@@ -372,7 +372,11 @@ def test_launch_counter_and_kernel_name(oracle):
     before = _lib.launch_count()
     device.encrypt_blocks(x, oracle.gen_keys(bytes(16)))
     assert _lib.launch_count() == before + 1
-    assert _lib.last_kernel().startswith("k_blocks_enc")
+    # 1024 blocks: the small-batch kernel (standard tables, texture S-box)
+    assert _lib.last_kernel() in ("k_blocks_small_enc", "k_blocks_enc_folded")
+    big = torch.zeros((1 << 20, 16), dtype=torch.uint8, device="cuda")
+    device.encrypt_blocks(big, oracle.gen_keys(bytes(16)))
+    assert _lib.last_kernel().startswith("k_blocks_enc_folded")
 
 
 @pytest.mark.parametrize("variant", [2])
