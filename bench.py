@@ -609,6 +609,33 @@ def openssl_rate(key: bytes, iv: bytes, budget_s: float = 2.0):
                       f"{budget_s:.0f} s each"}
 
 
+def openssl_sample_check(inp, p, out, cfg: int, n_sample: int = 1 << 16):
+    """(ok, blocks checked) for a seeded random sample of this rank's blocks
+    against OpenSSL AES-128-ECB of P ^ IV (per key for config 5), or None if
+    the `cryptography` package is missing."""
+    try:
+        from cryptography.hazmat.primitives.ciphers import Cipher, algorithms, modes
+    except ImportError:
+        return None
+    import torch
+    n = p.shape[0]
+    rows = np.sort(np.random.default_rng(SEED + 7).choice(n, min(n, n_sample), replace=False))
+    idx = torch.from_numpy(rows).to(p.device)
+    ph, ch = p[idx].cpu().numpy(), out[idx].cpu().numpy()
+    if cfg == 5:
+        kidx = rows // inp["bpk"]
+        ok = True
+        for k in np.unique(kidx):
+            sel = kidx == k
+            enc = Cipher(algorithms.AES(inp["keys"][k].tobytes()), modes.ECB()).encryptor()
+            want = np.frombuffer(enc.update((ph[sel] ^ inp["ivs"][k]).tobytes()), np.uint8).reshape(-1, 16)
+            ok &= bool(np.array_equal(want, ch[sel]))
+        return ok, int(rows.size)
+    enc = Cipher(algorithms.AES(inp["key"]), modes.ECB()).encryptor()
+    want = np.frombuffer(enc.update((ph ^ np.frombuffer(inp["iv"], np.uint8)).tobytes()), np.uint8).reshape(-1, 16)
+    return bool(np.array_equal(want, ch)), int(rows.size)
+
+
 def run_reference_impl(args):
     """--impl reference: the reference's stock CPU path, rank 0 only, on the
     same config / metric / unit as our arm; each step encrypts a bounded
@@ -1078,6 +1105,14 @@ def main(argv=None):
         back = device.many_key_decrypt(out, rk_dec, d_ivs)
     verified &= bool(torch.equal(back, p))
     check["round_trip"] = bool(torch.equal(back, p))
+    if cfg in (3, 4, 5):
+        # an independent implementation on a seeded sample of this rank's
+        # blocks: OpenSSL's AES-128-ECB of P ^ IV (pinned to the reference's
+        # config-1 digest in tests/test_gpu_fullsize.py); not the oracle
+        ossl = openssl_sample_check(inp, p, out, cfg)
+        if ossl is not None:
+            check["openssl_sample_blocks"] = ossl[1]
+            verified &= ossl[0]
 
     # decrypt throughput (reported, not the metric): same discipline
     def dstep():

@@ -285,7 +285,9 @@ inline bool nt_copies() {
 // Single-threaded piece of a staging copy (streaming stores when available).
 inline void stage_copy(void* dst, const void* src, size_t bytes) {
 #if defined(__x86_64__)
-  if (nt_copies() && bytes >= 4096) {
+  // (small pieces -- a small job's whole staging copy -- stay in the cache:
+  // measured faster for 16-160 KB jobs, scripts/r2/host_floor.cu)
+  if (nt_copies() && bytes >= ((size_t)64 << 10)) {
     nt_copy_avx2(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), bytes);
     return;
   }

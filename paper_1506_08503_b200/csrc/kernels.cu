@@ -231,14 +231,14 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
 // batch spreads evenly over the SMs.  The table fill reads only the kernel
 // parameters, so it runs before griddepcontrol.wait -- while the previous
 // launch on the stream is still computing, on the same SM (64 KiB and at
-// most 512 threads per CTA leave room for it).
+// most 512 threads per CTA leave room for it); the input is read only after
+// the wait (it may be the previous launch's output).
 template <bool DEC>
 __global__ void __launch_bounds__(kSmallThreads, 3)
     k_blocks_small(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks,
                    const __grid_constant__ SmallTables st, const __grid_constant__ RoundKeys rk,
                    cudaTextureObject_t tsb) {
   extern __shared__ __align__(1024) char smem[];
-  asm volatile("griddepcontrol.launch_dependents;");
   // region 0: entry x at 256 x, words 0-31 = T0[x] (32 lane copies), 32-63 = T1[x] = rotl8(T0[x])
   for (int q = threadIdx.x; q < 2 * 256 * 8; q += blockDim.x) {
     const int quad = q & 7, x = (q >> 3) & 255, tbl = q >> 11;
@@ -247,7 +247,13 @@ __global__ void __launch_bounds__(kSmallThreads, 3)
     *reinterpret_cast<uint4*>(smem + x * 256 + tbl * 128 + quad * 16) = make_uint4(v, v, v, v);
   }
   __syncthreads();
+  // The next launch may start (and fill its tables) once this one is past
+  // its own wait: triggering at the top let a chain of launches pile up on
+  // the SMs, their fills stealing shared-memory bandwidth from the lookups
+  // (config 1 as a ring of 20 launches: 4.92 us/step triggered at the top,
+  // 3.99 here, 5.63 at the end; profiles/r2/small_batches.md).
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const uint32_t lb = (threadIdx.x & 31) * 4;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
   uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -10,6 +10,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <chrono>
@@ -19,6 +20,18 @@
 #include "gaes_b200.h"
 
 __global__ void k_nop() {}
+
+// data arriving inside the launch (large kernel parameters, <= 32764 bytes)
+struct Big {
+  uint32_t n;
+  uint4 d[1000];
+};
+__global__ void k_param_copy(const __grid_constant__ Big p, uint4* out) {
+  for (uint32_t i = threadIdx.x + blockIdx.x * blockDim.x; i < p.n; i += gridDim.x * blockDim.x) out[i] = p.d[i];
+}
+__global__ void k_host_copy(const uint4* in, uint4* out, uint32_t n) {
+  for (uint32_t i = threadIdx.x + blockIdx.x * blockDim.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[i];
+}
 
 static double time_us(const std::function<void()>& f, int reps = 2000) {
   for (int i = 0; i < 200; i++) f();
@@ -53,6 +66,37 @@ int main() {
            cudaMemcpyAsync(hp, d, 16384, cudaMemcpyDeviceToHost, s);
            cudaStreamSynchronize(s);
          }));
+  {
+    static Big big;
+    big.n = 1000;
+    uint8_t *hin, *hout;
+    cudaMallocHost(&hin, 16000);
+    cudaMallocHost(&hout, 16000);
+    uint4 *din, *dout;
+    cudaHostGetDevicePointer((void**)&din, hin, 0);
+    cudaHostGetDevicePointer((void**)&dout, hout, 0);
+    printf("kernel copies 16 KB pinned->pinned (zero-copy) + sync: %.2f us\n", time_us([&] {
+             k_host_copy<<<8, 128, 0, s>>>(din, dout, 1000);
+             cudaStreamSynchronize(s);
+           }));
+    printf("kernel copies 16 KB from its parameters -> pinned + sync: %.2f us\n", time_us([&] {
+             k_param_copy<<<8, 128, 0, s>>>(big, dout);
+             cudaStreamSynchronize(s);
+           }));
+    printf("memcpy 16 KB into the param struct + the same: %.2f us\n", time_us([&] {
+             memcpy(big.d, h.data(), 16000);
+             k_param_copy<<<8, 128, 0, s>>>(big, dout);
+             cudaStreamSynchronize(s);
+           }));
+    printf("kernel writes 16 KB to pinned from device + sync: %.2f us\n", time_us([&] {
+             k_host_copy<<<8, 128, 0, s>>>((const uint4*)d, dout, 1000);
+             cudaStreamSynchronize(s);
+           }));
+    printf("kernel reads 16 KB pinned -> device + sync: %.2f us\n", time_us([&] {
+             k_host_copy<<<8, 128, 0, s>>>(din, (uint4*)d, 1000);
+             cudaStreamSynchronize(s);
+           }));
+  }
   cudaPointerAttributes a;
   printf("cudaPointerGetAttributes (pageable): %.3f us\n",
          time_us([&] { cudaPointerGetAttributes(&a, h.data()); }, 20000));
