@@ -349,7 +349,7 @@ GAES_API int gaes_cbc_encrypt_dev(const void* in, void* out, size_t n, size_t m,
                                   c->sms, (cudaStream_t)stream, tex_for(c, i8 + r * m, cnt * m, (cudaStream_t)stream),
                                   sbox_tex(c, c->d_std_enc)));
     }
-    note_kernel(last_rows_launch_used_tma() ? "k_cbc_enc_rows_tma" : "k_cbc_enc_rows");
+    note_kernel(last_rows_kernel());
   }
   return tmpo.finish();
 }

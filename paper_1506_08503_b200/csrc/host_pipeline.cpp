@@ -145,7 +145,7 @@ int launch_chunk(DevCtx* c, Lane* lane, const Job& j, cudaStream_t stream, const
     case Mode::kEncRows:
       GAES_CK(launch_cbc_enc_rows(in, out, rows, bpr, compact, j.rk, j.ivs ? ivs : nullptr, c->sms,
                                   stream, tin, tsb));
-      note_kernel(last_rows_launch_used_tma() ? "k_cbc_enc_rows_tma" : "k_cbc_enc_rows");
+      note_kernel(last_rows_kernel());
       break;
     case Mode::kManyKey: {
       const size_t kb = j.n_keys * 16, rkb = j.n_keys * 176;

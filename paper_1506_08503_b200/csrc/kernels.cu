@@ -358,6 +358,65 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
   }
 }
 
+// CBC encrypt along rows, four lanes per row: lane q of a quad owns state
+// column q.  Each lane looks up the four bytes of its own column; by
+// t_c = XOR_j T_j[s_{c+j}.b_j] the lookup T_j[s_q.b_j] belongs to column
+// q - j, so three shuffles per round hand the contributions to their
+// columns.  A round's critical path is one lookup plus one shuffle instead of
+// a thread's 16 dependent-issue lookups: for calls with too few rows to fill
+// the GPU (a few long messages), where one chain's latency is the whole cost
+// (_kernel.pyx:29-54).  A warp holds 8 rows; lanes of rows past the end run
+// the loop without loads or stores so the shuffles stay warp-uniform.
+__global__ void __launch_bounds__(kBlockThreads, 1)
+    k_cbc_enc_rows_quad(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t n_rows, uint64_t bpr,
+                        const uint32_t* __restrict__ compact, const __grid_constant__ RoundKeys rk,
+                        const uint32_t* __restrict__ ivs, cudaTextureObject_t tsb) {
+  extern __shared__ __align__(1024) char smem[];
+  pdl_prologue(smem, compact, tsb == 0);
+  const uint32_t lane = threadIdx.x & 31, q = lane & 3, quad0 = lane & ~3u;
+  const uint32_t lb = lane * 4;
+  const int l1 = (int)(quad0 | ((q + 1) & 3)), l2 = (int)(quad0 | ((q + 2) & 3)), l3 = (int)(quad0 | ((q + 3) & 3));
+  uint32_t k[11];
+#pragma unroll
+  for (int r = 0; r < 11; r++) k[r] = rk.w[4 * r + q];
+  const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g * 8 < n_rows; g += n_warps) {
+    const uint64_t row = g * 8 + (lane >> 2);
+    const bool live = row < n_rows;
+    uint32_t c = live ? (ivs ? __ldg(ivs + row * 4 + q) : rk.iv[q]) : 0u;
+    const uint32_t* src = in + row * bpr * 4 + q;
+    uint32_t* dst = out + row * bpr * 4 + q;
+    uint32_t p = live ? __ldg(src) : 0u;
+    for (uint64_t j = 0; j < bpr; j++) {
+      const uint32_t pn = (live && j + 1 < bpr) ? __ldg(src + (j + 1) * 4) : 0u;
+      uint32_t st = p ^ c ^ k[0];
+#pragma unroll
+      for (int r = 1; r < 10; r++) {
+        const uint32_t u0 = lds_u32(smem, taddr<0>(st, lb), kOffT0), u1 = lds_u32(smem, taddr<1>(st, lb), kOffT1);
+        const uint32_t u2 = lds_u32(smem, taddr<2>(st, lb), kOffT2), u3 = lds_u32(smem, taddr<3>(st, lb), kOffT3);
+        st = u0 ^ __shfl_sync(0xFFFFFFFFu, u1, l1) ^ __shfl_sync(0xFFFFFFFFu, u2, l2) ^
+             __shfl_sync(0xFFFFFFFFu, u3, l3) ^ k[r];
+      }
+      uint32_t v0, v1, v2, v3;  // S[byte j of this column], placed at byte j
+      if (tsb) {
+        v0 = tex_sbox(tsb, st & 0xFF);
+        v1 = tex_sbox(tsb, (st >> 8) & 0xFF) << 8;
+        v2 = tex_sbox(tsb, (st >> 16) & 0xFF) << 16;
+        v3 = tex_sbox(tsb, st >> 24) << 24;
+      } else {
+        v0 = lds_u32(smem, taddr<0>(st, lb), kOffS);
+        v1 = lds_u32(smem, taddr<1>(st, lb), kOffS) << 8;
+        v2 = lds_u32(smem, taddr<2>(st, lb), kOffS) << 16;
+        v3 = lds_u32(smem, taddr<3>(st, lb), kOffS) << 24;
+      }
+      c = v0 ^ __shfl_sync(0xFFFFFFFFu, v1, l1) ^ __shfl_sync(0xFFFFFFFFu, v2, l2) ^
+          __shfl_sync(0xFFFFFFFFu, v3, l3) ^ k[10];
+      if (live) __stcs(dst + j * 4, c);
+      p = pn;
+    }
+  }
+}
+
 // CBC encrypt along rows with the row tiles staged through shared memory by
 // TMA.  A warp owns 32 consecutive rows (lane = row, serial chain per row,
 // _kernel.pyx:29-54); per step it needs the next 2 blocks (32 bytes) of each
@@ -858,8 +917,8 @@ static void rows_geometry(uint64_t n_rows, int sms, int* grid, int* threads) {
   *grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(sms, (per_wave + t - 1) / t));
 }
 
-static thread_local bool t_rows_tma = false;
-bool last_rows_launch_used_tma() { return t_rows_tma; }
+static thread_local const char* t_rows_kernel = "k_cbc_enc_rows";
+const char* last_rows_kernel() { return t_rows_kernel; }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no link
 // dependency on libcuda); nullptr if unavailable.
@@ -939,8 +998,22 @@ cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint
   {
     bool launched = false;
     cudaError_t e = launch_cbc_enc_rows_tma(in, out, n_rows, bpr, compact, rk, ivs, sms, s, tsb, &launched);
-    t_rows_tma = launched;
+    t_rows_kernel = launched ? "k_cbc_enc_rows_tma" : "k_cbc_enc_rows";
     if (e != cudaSuccess || launched) return e;
+  }
+  // Too few rows to give every SM a full set of chains: the per-row chain
+  // latency is the whole cost -- four lanes per row (k_cbc_enc_rows_quad).
+  if (n_rows * 4 <= (uint64_t)sms * kBlockThreads && bpr > 1 &&
+      ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(ivs)) & 3) == 0 &&
+      rt::tune_int("ROWS_QUAD", 1) != 0) {
+    cudaError_t e = set_smem(k_cbc_enc_rows_quad);
+    if (e != cudaSuccess) return e;
+    const uint64_t per_sm = (n_rows + sms - 1) / sms;
+    const int threads = (int)std::min<uint64_t>(kBlockThreads, std::max<uint64_t>(32, (per_sm * 4 + 31) & ~(uint64_t)31));
+    const int grid = (int)((n_rows * 4 + threads - 1) / threads);
+    t_rows_kernel = "k_cbc_enc_rows_quad";
+    return launch_pdl(k_cbc_enc_rows_quad, grid, threads, kSmemBytes, s, (const uint32_t*)in, (uint32_t*)out, n_rows,
+                      bpr, compact, rk, (const uint32_t*)ivs, tsb);
   }
   const bool pairs = bpr >= 2 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 31) == 0 &&
                      (bpr % 2 == 0);

@@ -36,8 +36,9 @@ uint64_t small_blocks_max(int sms);
 cudaError_t launch_blocks_small(bool dec, const void* in, void* out, uint64_t n_blocks, const uint32_t* t0,
                                 const RoundKeys& rk, int sms, cudaStream_t s, cudaTextureObject_t tsb);
 // Row CBC encrypt: the TMA-staged kernel when it applies (texture S-box,
-// >= 8 even blocks per row, enough rows), else the LDG/STG kernel.
-bool last_rows_launch_used_tma();  // on this thread
+// >= 8 even blocks per row, enough rows), four lanes per row when there are
+// too few rows to fill the GPU, else the LDG/STG kernel.
+const char* last_rows_kernel();  // which row-CBC encrypt kernel the last launch on this thread used
 cudaError_t launch_cbc_enc_rows(const void* in, void* out, uint64_t n_rows, uint64_t bpr, const uint32_t* compact,
                                 const RoundKeys& rk, const void* ivs, int sms, cudaStream_t s,
                                 cudaTextureObject_t tin = 0, cudaTextureObject_t tsb = 0);

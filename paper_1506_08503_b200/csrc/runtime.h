@@ -34,7 +34,7 @@ int env_int(const char* name, int dflt);
 // Measurement-only overrides of the settled tuning choices, all through one
 // variable: GAES_TUNE="KEY=VALUE,KEY=VALUE" (keys: PDL, EARLY, ILP, TEXS,
 // TEXIN, ROWS_TMA, ROWS_TMA_MIN_GROUPS, NT, MEMCPY_GRAIN_KB, ZEROCOPY_MB,
-// SMALL_ZEROCOPY_KB, SMALL_BLOCKS_PER_SM, CHUNK_MB, PAGEABLE_CHUNK_MB,
+// SMALL_ZEROCOPY_KB, SMALL_BLOCKS_PER_SM, ROWS_QUAD, CHUNK_MB, PAGEABLE_CHUNK_MB,
 // LANES).  Unset in normal
 // use: the defaults are the measured choices.  Returns `dflt`
 // for keys not given.
