@@ -799,8 +799,11 @@ def roofline_for(args, n, ms_local, clocks, dev, local, step, launches):
         pass
     peak = lds_measured or lds_peak
     per_step = max(1, launches // max(1, args.steps))
+    step()
+    torch.cuda.synchronize()
+    kernel = _lib.last_kernel()  # the step's kernel: k_blocks (large batches), k_blocks_small, k_many_key
     return {
-        "bound": "smem", "kernel": "k_blocks_enc_folded" if args.config != 5 else "k_many_key_enc",
+        "bound": "smem", "kernel": kernel,
         "achieved": round(lds_achieved, 2), "peak": round(peak, 2), "unit": "Glookup/s",
         "frac": round(lds_achieved / peak, 4), "traffic": traffic,
         "traffic_unit": "GB per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, profiles/traffic.json)",
