@@ -159,3 +159,29 @@ def test_reference_cpu_matches_the_oracle_and_round_trips():
     r.decrypt()
     r.check()
     assert np.array_equal(r.back, r.p)
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_openssl_sample_check_catches_a_wrong_block(monkeypatch, cfg):
+    """bench.py's in-run independent check (OpenSSL ECB of P ^ IV on a seeded
+    sample) accepts the oracle's ciphertext and rejects a corrupted one."""
+    pytest.importorskip("cryptography")
+    import torch
+
+    import bench
+    from oracle import oracle
+    monkeypatch.setattr(bench, "GEN_CHUNK_BLOCKS", 1 << 12)
+    blocks = 1024 * 8 if cfg == 5 else 1 << 13
+    inp = bench.make_inputs(cfg, 0, 1, torch.device("cpu"), blocks=blocks)
+    p = inp["p"].numpy()
+    if cfg == 5:
+        bpk = inp["bpk"]
+        c = np.concatenate([oracle.encrypt(inp["keys"][k].tobytes(), np.tile(inp["ivs"][k], (bpk, 1)),
+                                           p[k * bpk:(k + 1) * bpk]) for k in range(inp["keys"].shape[0])])
+    else:
+        c = oracle.encrypt(inp["key"], np.tile(np.frombuffer(inp["iv"], np.uint8), (blocks, 1)), p)
+    out = torch.from_numpy(c.copy())
+    ok, n = bench.openssl_sample_check(inp, inp["p"], out, cfg, n_sample=blocks)
+    assert ok and n == blocks
+    out[blocks // 2, 3] ^= 1
+    assert not bench.openssl_sample_check(inp, inp["p"], out, cfg, n_sample=blocks)[0]
