@@ -301,8 +301,10 @@ def cpu_sample(cfg: int, n: int) -> tuple:
         p = np.zeros((n, 16), np.uint8)
         p[:, :8] = prm["vals"][r].view(np.uint8).reshape(n, 8)
         return p, [(key, iv, 0, n)]
-    # cfg 5: the first keys, each with an equal share of the sample
-    nk = max(1, min(WORKLOADS[5]["keys"], n // 4096))
+    # cfg 5: the first keys, each with the workload's 2^20 blocks (fewer for
+    # a sample below one key's share) -- the per-key call the reference makes
+    per_key = (1 << 30) // WORKLOADS[5]["keys"]
+    nk = max(1, min(WORKLOADS[5]["keys"], n // per_key))
     per = max(1, n // nk)
     p = rng.integers(0, 256, (nk * per, 16), dtype=np.uint8)
     return p, [(prm["keys"][i].tobytes(), prm["ivs"][i].tobytes(), i * per, (i + 1) * per) for i in range(nk)]

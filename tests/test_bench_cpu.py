@@ -123,7 +123,10 @@ def test_cpu_sample_follows_the_workload(cfg):
     if cfg != 5:
         assert segs == [(prm["key"], prm["iv"], 0, p.shape[0])]
     else:
-        assert segs[0][0] == prm["keys"][0].tobytes() and len(segs) == 2
+        assert segs[0][0] == prm["keys"][0].tobytes() and len(segs) == 1
+        p2, segs2 = bench.cpu_sample(cfg, 1 << 21)  # two keys' worth of the workload's 2^20 blocks
+        assert [(a, b) for _, _, a, b in segs2] == [(0, 1 << 20), (1 << 20, 1 << 21)]
+        assert segs2[1][0] == prm["keys"][1].tobytes() and segs2[1][1] == prm["ivs"][1].tobytes()
     if cfg == 4:
         assert not p[:, 8:].any()
 
