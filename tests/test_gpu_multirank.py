@@ -119,3 +119,18 @@ def test_two_ranks_strong_scaling_config5_keys_sharded():
     got = [(d["blocks"], d["sha256"]) for d in line["digests"]]
     assert [b for b, _ in got] == [list(p) for p in bench.pieces(5)]
     assert got == [(list(b), h) for b, h in _single_rank_piece_digests(5)]
+
+
+def test_one_rank_under_torchrun_uses_nccl_plumbing():
+    """The driver's N > 1 layout (one rank per GPU) takes the NCCL branch:
+    init with device_id, barriers, the MAX reductions on CUDA tensors and
+    the all_gather_object of the digests.  One rank on this GPU exercises
+    exactly that code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "1",
+           "--config", "3", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e"]
+    r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-5000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["dist"]["backend"] == "nccl" and line["n_gpus"] == 1 and line["verified"] is True
+    assert [d["blocks"] for d in line["digests"]] == [list(p) for p in bench.pieces(3)]
