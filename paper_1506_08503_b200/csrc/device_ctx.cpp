@@ -430,22 +430,22 @@ int ilp_default() {
 }
 
 cudaError_t launch_enc_folded(DevCtx* c, const void* in, void* out, uint64_t n, const uint32_t* compact,
-                              const RoundKeys& k, int ilp, cudaStream_t s, cudaTextureObject_t tin) {
+                              const RoundKeys& k, int ilp, cudaStream_t s, cudaTextureObject_t tin, bool host_job) {
   if (g_variant.load() == 2) {
     static thread_local BitsliceKeys bk;
     bs_make_keys(k.w, bk);
     note_kernel("k_bs_blocks");
     return launch_bs_blocks(in, out, n, bk, c->sms, s);
   }
-  return launch_folded(c, false, in, out, n, compact, k, s, tin);
+  return launch_folded(c, false, in, out, n, compact, k, s, tin, host_job);
 }
 
 cudaError_t launch_folded(DevCtx* c, bool dec, const void* in, void* out, uint64_t n, const uint32_t* compact,
-                          const RoundKeys& k, cudaStream_t s, cudaTextureObject_t tin) {
+                          const RoundKeys& k, cudaStream_t s, cudaTextureObject_t tin, bool host_job) {
   const cudaTextureObject_t tsb = sbox_tex(c, compact);  // nonzero only for the GF layer's tables
   if (tsb && n <= small_blocks_max(c->sms) && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
     note_kernel(dec ? "k_blocks_small_dec" : "k_blocks_small_enc");
-    return launch_blocks_small(dec, in, out, n, dec ? c->std_td : c->std_te, k, c->sms, s, tsb);
+    return launch_blocks_small(dec, in, out, n, dec ? c->std_td : c->std_te, k, c->sms, s, tsb, host_job);
   }
   note_kernel(dec ? "k_blocks_dec_folded" : (tsb ? "k_blocks_enc_folded+texsbox" : "k_blocks_enc_folded"));
   return launch_blocks(dec, kIvFolded, ilp_default(), in, out, n, compact, k, nullptr, 1, c->sms, s, tin, 0, tsb);

@@ -283,13 +283,15 @@ int ilp_default();
 cudaTextureObject_t sbox_tex(const DevCtx* c, const uint32_t* compact);
 // M = 16 shared-IV encrypt: the formulation chosen by measurement
 // (profiles/): T-table unless gaes_set_variant(2) selects the bitsliced kernel.
+// host_job: a synchronous host-buffer job (see launch_blocks_small's `early`).
 cudaError_t launch_enc_folded(DevCtx* c, const void* in, void* out, uint64_t n, const uint32_t* compact,
-                              const RoundKeys& k, int ilp, cudaStream_t s, cudaTextureObject_t tin);
+                              const RoundKeys& k, int ilp, cudaStream_t s, cudaTextureObject_t tin,
+                              bool host_job = false);
 
 // M = 16 with the IV folded into the key (either direction): the small-batch
 // kernel for standard tables and n <= small_blocks_max, else k_blocks.
 cudaError_t launch_folded(DevCtx* c, bool dec, const void* in, void* out, uint64_t n, const uint32_t* compact,
-                          const RoundKeys& k, cudaStream_t s, cudaTextureObject_t tin);
+                          const RoundKeys& k, cudaStream_t s, cudaTextureObject_t tin, bool host_job = false);
 
 // Runs fn(offset, count) over [0, n) in texture-sized segments.
 template <typename F>

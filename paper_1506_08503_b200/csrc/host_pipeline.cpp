@@ -127,10 +127,10 @@ int launch_chunk(DevCtx* c, Lane* lane, const Job& j, cudaStream_t stream, const
   switch (j.mode) {
     case Mode::kFolded:
       if (j.dec) {
-        GAES_CK(launch_folded(c, true, in, out, nblk, compact, j.rk, stream, tin));
+        GAES_CK(launch_folded(c, true, in, out, nblk, compact, j.rk, stream, tin, /*host_job=*/true));
       } else if (j.standard || g_variant.load() < 2) {
-        GAES_CK(launch_enc_folded(c, in, out, nblk, compact, j.rk, ilp_default(), stream,
-                                  tin));
+        GAES_CK(launch_enc_folded(c, in, out, nblk, compact, j.rk, ilp_default(), stream, tin,
+                                  /*host_job=*/true));
       } else {  // bitsliced kernel has the standard S-box built in; caller tables -> T-table
         GAES_CK(launch_blocks(false, kIvFolded, ilp_default(), in, out, nblk, compact, j.rk, nullptr, 1,
                               c->sms, stream, 0, 0, tsb));

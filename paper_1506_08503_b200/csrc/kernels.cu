@@ -237,8 +237,19 @@ template <bool DEC>
 __global__ void __launch_bounds__(kSmallThreads, 3)
     k_blocks_small(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_blocks,
                    const __grid_constant__ SmallTables st, const __grid_constant__ RoundKeys rk,
-                   cudaTextureObject_t tsb) {
+                   cudaTextureObject_t tsb, int early) {
   extern __shared__ __align__(1024) char smem[];
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint4 cur = make_uint4(0, 0, 0, 0);
+  // early (a synchronous host-buffer job: nothing in flight on the stream
+  // to overlap the fill with): wait first and put the input load in flight
+  // before the fill, so its latency (PCIe for host memory) hides behind it
+  if (early) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (b < n_blocks) cur = ld_stream(in + b);
+  }
   // region 0: entry x at 256 x, words 0-31 = T0[x] (32 lane copies), 32-63 = T1[x] = rotl8(T0[x])
   for (int q = threadIdx.x; q < 2 * 256 * 8; q += blockDim.x) {
     const int quad = q & 7, x = (q >> 3) & 255, tbl = q >> 11;
@@ -252,13 +263,12 @@ __global__ void __launch_bounds__(kSmallThreads, 3)
   // the SMs, their fills stealing shared-memory bandwidth from the lookups
   // (config 1 as a ring of 20 launches: 4.92 us/step triggered at the top,
   // 3.99 here, 5.63 at the end; profiles/r2/small_batches.md).
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;");
+  if (!early) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (b < n_blocks) cur = ld_stream(in + b);
+  }
   const uint32_t lb = (threadIdx.x & 31) * 4;
-  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
-  uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= n_blocks) return;
-  uint4 cur = ld_stream(in + b);
   while (b < n_blocks) {
     const uint64_t nb = b + T;
     uint4 nxt = cur;
@@ -887,7 +897,7 @@ uint64_t small_blocks_max(int sms) {
 }
 
 cudaError_t launch_blocks_small(bool dec, const void* in, void* out, uint64_t n, const uint32_t* t0,
-                                const RoundKeys& rk, int sms, cudaStream_t s, cudaTextureObject_t tsb) {
+                                const RoundKeys& rk, int sms, cudaStream_t s, cudaTextureObject_t tsb, bool early) {
   if (n == 0) return cudaSuccess;
   auto kern = dec ? k_blocks_small<true> : k_blocks_small<false>;
   cudaError_t e = set_smem(kern, kSmallSmemBytes);
@@ -899,7 +909,8 @@ cudaError_t launch_blocks_small(bool dec, const void* in, void* out, uint64_t n,
   uint64_t per_sm = (n + sms - 1) / sms;
   int threads = (int)std::min<uint64_t>(kSmallThreads, std::max<uint64_t>(128, (per_sm + 31) & ~(uint64_t)31));
   const uint64_t ctas = std::min<uint64_t>((uint64_t)3 * sms, (n + threads - 1) / threads);
-  return launch_pdl(kern, (int)ctas, threads, kSmallSmemBytes, s, (const uint4*)in, (uint4*)out, n, st, rk, tsb);
+  return launch_pdl(kern, (int)ctas, threads, kSmallSmemBytes, s, (const uint4*)in, (uint4*)out, n, st, rk, tsb,
+                    early ? 1 : 0);
 }
 
 // Row-CBC geometry: a thread owns whole rows, so the launch is sized in

@@ -33,8 +33,11 @@ cudaError_t launch_blocks(bool dec, int ivmode, int ilp, const void* in, void* o
 // k_blocks_small -- 64 KiB of tables filled from the kernel parameters, up
 // to 3 CTAs per SM so the next launch fills while this one computes.
 uint64_t small_blocks_max(int sms);
+// early: the caller's stream has nothing in flight to overlap the fill with
+// (synchronous host-buffer jobs): load the input first, then fill.
 cudaError_t launch_blocks_small(bool dec, const void* in, void* out, uint64_t n_blocks, const uint32_t* t0,
-                                const RoundKeys& rk, int sms, cudaStream_t s, cudaTextureObject_t tsb);
+                                const RoundKeys& rk, int sms, cudaStream_t s, cudaTextureObject_t tsb,
+                                bool early = false);
 // Row CBC encrypt: the TMA-staged kernel when it applies (texture S-box,
 // >= 8 even blocks per row, enough rows), four lanes per row when there are
 // too few rows to fill the GPU, else the LDG/STG kernel.
