@@ -202,7 +202,7 @@ GAES_API int gaes_probe_round_rate(int device, uint32_t iters, double *lookups_p
 GAES_API int gaes_probe_lds_peak(int device, uint32_t iters, double *lookups_per_sec, double *ms);
 /* 1 if the standard-table kernels on `device` read round 10's S-box through
  * the texture path (144 shared-memory lookups + 16 texture fetches per
- * block), 0 if all 160 lookups are shared-memory (GAES_TEXS=0), < 0 on
+ * block), 0 if all 160 lookups are shared-memory (GAES_TUNE=TEXS=0), < 0 on
  * error.  Tells the roofline which lookups the L1/shared data pipe serves. */
 GAES_API int gaes_uses_sbox_texture(int device);
 /* Select the M=16 encrypt/decrypt formulation: 0 = auto (fastest measured),

@@ -251,7 +251,7 @@ unsigned long long buffer_id(const void* p) {
 // staging slots reuse buffers, and a buffer freed and re-allocated at the
 // same address is a different allocation, whose old texture object must not
 // be reused (it was created over memory that no longer exists).  Empty
-// (handle 0) when disabled (GAES_TEXIN=0), misaligned, too large or
+// (handle 0) when disabled (GAES_TUNE=TEXIN=0), misaligned, too large or
 // unavailable -- the kernels then use LDG.  Must be called with c->dev
 // current and the lease used for one launch on `stream`.  At 64 entries the
 // least recently used idle entry is evicted after waiting for the launches

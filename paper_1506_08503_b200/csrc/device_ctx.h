@@ -107,7 +107,7 @@ struct DevCtx {
   uint8_t* d_tmp = nullptr;      // GF-build outputs + error flag
   // S-box / inverse S-box bytes (256 B each) and u8 textures over them: the
   // last round's lookups for the standard tables go through the TEX pipe
-  // (0 = unavailable or GAES_TEXS=0: read the replicated S table in smem)
+  // (0 = unavailable or GAES_TUNE=TEXS=0: read the replicated S table in smem)
   uint8_t* d_sbox = nullptr;
   uint8_t* d_inv = nullptr;
   cudaTextureObject_t tex_s_enc = 0, tex_s_dec = 0;
