@@ -250,10 +250,17 @@ __global__ void __launch_bounds__(kSmallThreads, 3)
     asm volatile("griddepcontrol.launch_dependents;");
     if (b < n_blocks) cur = ld_stream(in + b);
   }
-  // region 0: entry x at 256 x, words 0-31 = T0[x] (32 lane copies), 32-63 = T1[x] = rotl8(T0[x])
+  // T0 from the parameters into shared memory in one pass (every constant
+  // load in flight at once -- a CTA of 128 threads walking the replication
+  // loop would take its constant-cache misses one after another), then
+  // region 0: entry x at 256 x, words 0-31 = T0[x] (32 lane copies), 32-63 =
+  // T1[x] = rotl8(T0[x])
+  __shared__ uint32_t t0s[256];
+  for (int x = threadIdx.x; x < 256; x += blockDim.x) t0s[x] = st.t0[x];
+  __syncthreads();
   for (int q = threadIdx.x; q < 2 * 256 * 8; q += blockDim.x) {
     const int quad = q & 7, x = (q >> 3) & 255, tbl = q >> 11;
-    const uint32_t t = st.t0[x];
+    const uint32_t t = t0s[x];
     const uint32_t v = tbl ? __funnelshift_l(t, t, 8) : t;
     *reinterpret_cast<uint4*>(smem + x * 256 + tbl * 128 + quad * 16) = make_uint4(v, v, v, v);
   }
