@@ -177,7 +177,7 @@ bool stage_and_check_iv(uint8_t* dst, const uint8_t* src, size_t m, const uint8_
   uint64_t a0, a1;
   std::memcpy(&a0, iv0, 8);
   std::memcpy(&a1, iv0 + 8, 8);
-  parallel_ranges(rows, std::max<size_t>(1, ((size_t)128 << 10) / m), [&](size_t lo, size_t hi) {
+  parallel_ranges(rows, std::max<size_t>(1, copy_grain() / m), [&](size_t lo, size_t hi) {
     stage_copy(dst + lo * m, src + lo * m, (hi - lo) * m);
     if (!same.load(std::memory_order_relaxed)) return;
     uint64_t diff = 0;

@@ -295,9 +295,14 @@ inline void stage_copy(void* dst, const void* src, size_t bytes) {
   std::memcpy(dst, src, bytes);
 }
 
+// Minimum bytes per copy thread of a parallel staging copy.
+inline size_t copy_grain() {
+  static const size_t grain = (size_t)std::max(4, rt::tune_int("MEMCPY_GRAIN_KB", 128)) << 10;
+  return grain;
+}
+
 inline void par_memcpy(void* dst, const void* src, size_t bytes) {
-  static const size_t grain = (size_t)std::max(16, rt::tune_int("MEMCPY_GRAIN_KB", 128)) << 10;
-  parallel_ranges(bytes, grain, [&](size_t lo, size_t hi) {
+  parallel_ranges(bytes, copy_grain(), [&](size_t lo, size_t hi) {
     stage_copy((uint8_t*)dst + lo, (const uint8_t*)src + lo, hi - lo);
   });
 }
