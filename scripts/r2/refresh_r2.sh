@@ -10,6 +10,7 @@ st() { echo "$1 rc=$2" | tee -a $O/status.txt; }
 timeout 1800 python -m pytest tests -q -m gpu > $O/pytest_gpu.log 2>&1; st pytest $?
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; st smoke $?
 python bench.py > $O/bench_default.json 2> $O/bench_default.err; st bench $?
+for r in 2 3; do python bench.py --no-cpu-baseline > $O/bench_default_rep$r.json 2> $O/bench_default_rep$r.err; st bench_rep$r $?; done
 python bench.py --impl reference > $O/bench_reference_arm.json 2> $O/bench_reference_arm.err; st ref $?
 for c in 1 2 4 5; do
   python bench.py --config $c > $O/bench_cfg$c.json 2> $O/bench_cfg$c.err; st cfg$c $?
@@ -22,6 +23,8 @@ $CMD > $O/plain_default2.json 2>&1 && \
 CMD1="python bench.py --config 1 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e"
 $CMD1 > $O/plain_cfg1.json 2>&1 && \
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/launches_cfg1.csv $CMD1 > $O/ncu_launches1.log 2>&1; st ncu_launches_cfg1 $?
+$CMD1 > $O/plain_cfg1b.json 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:k_blocks_small -s 12 -c 1 -o $O/small_cfg1 $CMD1 > $O/ncu_small.log 2>&1; st ncu_small $?
 python scripts/profile_kernels.py cbc_rows 20 4096 > $O/plain_quad.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:k_cbc_enc_rows_quad -s 2 -c 1 -o $O/rows_quad python scripts/profile_kernels.py cbc_rows 20 4096 > $O/ncu_quad.log 2>&1; st ncu_quad $?
 for c in 3 4 5; do
