@@ -266,3 +266,40 @@ def test_concurrent_callers_with_the_new_pool(oracle):
     [t.start() for t in th]
     [t.join() for t in th]
     assert not errors
+
+
+def test_sharded_calls_from_many_threads():
+    """Six caller threads on the 2-shard path at once (more callers than a
+    device's 4 runner threads / lanes): every result bit-exact, no deadlock."""
+    code = r'''
+import sys, threading, numpy as np
+sys.path.insert(0, ".")
+from oracle import oracle
+from paper_1506_08503_b200 import _lib, backend_cuda
+assert _lib.set_num_gpus(2) == 2
+rng = np.random.default_rng(11)
+key = rng.bytes(16)
+tables = oracle.encrypt_tables(key)
+jobs = []
+for t in range(6):
+    n = 50000 + 977 * t
+    p = rng.integers(0, 256, (n, 32), dtype=np.uint8)
+    ivs = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    jobs.append((p, ivs, oracle.encrypt(key, ivs, p, threads=2)))
+bad = []
+def work(t):
+    p, ivs, want = jobs[t]
+    for _ in range(5):
+        out = np.empty_like(p)
+        backend_cuda.cbc_encrypt(p, ivs, *tables, out)
+        if not np.array_equal(out, want):
+            bad.append(t)
+th = [threading.Thread(target=work, args=(t,)) for t in range(6)]
+[x.start() for x in th]
+[x.join() for x in th]
+assert not bad, bad
+print("ok", _lib.debug_counters()["shard_runner_threads"])
+'''
+    env = dict(os.environ, GAES_DEVICE_MAP="0,0")
+    r = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
