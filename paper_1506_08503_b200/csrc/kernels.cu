@@ -5,9 +5,13 @@
 //   k_blocks            M = 16 blocks, per-message IVs and block-parallel CBC
 //                       decrypt: T tables in shared memory (rounds 1-9), S-box
 //                       through a texture (round 10), inputs through textures
+//   k_blocks_small      M = 16, small batches: T0|T1 from the kernel parameters
+//                       (T2/T3 as 16-bit rotations), fills before the PDL wait
 //   k_cbc_enc_rows_tma  CBC encrypt along rows (serial chain, M > 16) with the
 //                       row tiles staged through shared memory by TMA
-//   k_cbc_enc_rows      the same with per-lane 256-bit LDG/STG (few long rows)
+//   k_cbc_enc_rows      the same with per-lane 256-bit LDG/STG
+//   k_cbc_enc_rows_quad the same with four lanes per row (too few rows to fill
+//                       the GPU: chain latency bound)
 //   k_generic_cbc       byte-level round for arbitrary shift permutations /
 //                       non-linear mix tables (correctness path, still GPU)
 //   k_expand_keys       batched key schedule (key_schedule.py:50-70)
