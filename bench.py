@@ -1069,7 +1069,7 @@ def main(argv=None):
     ms_step = max_over_ranks(ms_local, reduce_dev)
     job_blocks = n * world if weak else total_blocks(cfg, world)
     value = job_blocks * BYTES_PER_BLOCK / (ms_step / 1e3) / 1e9
-    wall_span = {"ms_per_step": round(span_s * 1e3 / args.steps, 4),
+    wall_span = {"ms_per_step": round(span_s * 1e3 / args.steps, 6),
                  "value": round(job_blocks * BYTES_PER_BLOCK * args.steps / span_s / 1e9, 2), "unit": "GB/s",
                  "note": ("host barrier -> last rank's completion of K steps (host monotonic clock, all ranks); "
                           + ("one graph replay of the K-step ring" if graph is not None else "back-to-back steps"))}
