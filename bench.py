@@ -512,8 +512,12 @@ def cpu_baseline(cfg: int, budget_s: float):
     rate = _cpu_rate_probe(cfg, threads)
     n = int(min(CPU_SAMPLE_CAP, max(1 << 16, rate * budget_s / 8)))
     r = ReferenceCPU(cfg, n, threads)
-    enc = r.timed(r.encrypt, 4, 1)
-    dec = r.timed(r.decrypt, 2, 0)
+    # ~budget_s of CPU work in all: as many encrypt repetitions as ~60 % of
+    # the budget holds (4..40), half as many decrypt ones
+    t_one = r.timed(r.encrypt, 1, 1)[0]
+    reps = int(max(4, min(40, 0.6 * budget_s / max(t_one, 1e-6))))
+    enc = r.timed(r.encrypt, reps, 0)
+    dec = r.timed(r.decrypt, max(2, reps // 2), 0)
     r.check()
     assert np.array_equal(r.back, r.p), "CPU reference round trip failed"
     one = ReferenceCPU(cfg, 1 << 18, 1)
@@ -526,10 +530,11 @@ def cpu_baseline(cfg: int, budget_s: float):
     gbs = lambda ts, m: round(m * BYTES_PER_BLOCK / statistics.median(ts) / 1e9, 4)  # noqa: E731
     return {"value": gbs(enc, r.n), "unit": "GB/s", "cores": threads, "kind": r.kind,
             "sample": (f"{r.n} blocks of the workload (first blocks of its generator recipe, numpy draws), median of "
-                       f"4 reps, {threads} threads over parallel.plan chunks, parallel._run_chunks"),
+                       f"{len(enc)} reps, {threads} threads over parallel.plan chunks, parallel._run_chunks; "
+                       f"{sum(enc) + sum(dec):.1f} s wall on {threads} threads"),
             "source": r.source,
             "decrypt": {"value": gbs(dec, r.n), "unit": "GB/s", "cores": threads,
-                        "sample": f"the same {r.n} blocks, median of 2 reps (cbc_decrypt, _decrypt_tables)"},
+                        "sample": f"the same {r.n} blocks, median of {len(dec)} reps (cbc_decrypt, _decrypt_tables)"},
             "single_thread": {"value": gbs(t1, one.n), "unit": "GB/s", "sample": f"{one.n} blocks, 1 thread"},
             "logical_cpus": threads, "physical_cores": physical}
 
