@@ -218,3 +218,55 @@ def test_pyfast_defers_every_irregular_argument_to_the_checked_path():
         backend_cuda.cbc_encrypt(d.view(np.int8), iv, rk, box, lut, perm, out)
     with pytest.raises(ValueError, match="read-only"):
         backend_cuda.cbc_encrypt(d, iv, rk, box, lut, perm, np.frombuffer(bytes(256), np.uint8).reshape(8, 32))
+
+
+def test_pyfast_never_crashes_on_random_arguments():
+    """Random shapes, dtypes, strides and non-arrays for every argument: the
+    fast path either returns None (irregular input -> Python checks) or a
+    return code; it never raises, crashes or accepts an irregular buffer."""
+    hypothesis = pytest.importorskip("hypothesis")
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    from paper_1506_08503_b200 import _pyfast
+
+    def arr(draw, shape):
+        kind = draw(st.sampled_from(["ok", "dtype", "shape", "strided", "readonly", "list", "bytes"]))
+        if kind == "ok":
+            return np.zeros(shape, np.uint8), True
+        if kind == "dtype":
+            return np.zeros(shape, draw(st.sampled_from([np.int8, np.uint16, np.float32, np.bool_]))), False
+        if kind == "shape":
+            return np.zeros(tuple(s + draw(st.integers(1, 3)) for s in shape), np.uint8), False
+        if kind == "strided":
+            big = np.zeros(tuple(2 * s for s in shape), np.uint8)
+            return big[tuple(slice(None, None, 2) for _ in shape)], False
+        if kind == "readonly":
+            a = np.zeros(shape, np.uint8)
+            a.setflags(write=False)
+            return a, None  # fine as an input, not as `out`
+        if kind == "list":
+            return [0] * int(np.prod(shape)), False
+        return bytes(int(np.prod(shape))), None
+
+    @st.composite
+    def call(draw):
+        n = draw(st.integers(1, 5))
+        m = 16 * draw(st.integers(1, 3))
+        shapes = [(n, m), (n, 16), (11, 16), (256,), (4, 4, 256), (16,), (n, m)]
+        return [arr(draw, s) for s in shapes]
+
+    @settings(max_examples=300, deadline=None)
+    @given(call())
+    def check(args):
+        vals = [a for a, _ in args]
+        oks = [ok for _, ok in args]
+        vals[5] = np.arange(16, dtype=np.uint8) if oks[5] is True else vals[5]
+        rc = _pyfast.cbc(False, *vals)
+        regular = all(ok is True for ok in oks[:6]) and oks[6] is True
+        if not regular and not (oks[6] is True and all(ok in (True, None) for ok in oks[:6])):
+            assert rc is None
+        if rc is not None:
+            assert isinstance(rc, int)
+
+    check()
