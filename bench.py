@@ -1003,7 +1003,6 @@ def main(argv=None):
         torch.cuda.synchronize()
         mark = clk.mark()
         t_timed = time.perf_counter()
-        launches0 = _lib.launch_count()
         if graph is not None:
             flush.fill_(1)  # evicts the whole ring (and keeps the GPU busy while the host enqueues)
             starts[0].record(stream)
